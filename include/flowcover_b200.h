@@ -1,0 +1,238 @@
+/*
+ * flowcover_b200.h -- C ABI of the B200-native reference-flow generator.
+ *
+ * Drop-in boundary for the hot path of the reference package `flowcover`
+ * (/root/reference/pkg/src/flowcover).  Each entry point below replaces one
+ * reference Python function; the citation names the function it replaces.
+ * The Python layer (paper_2511_11514_b200/*.py) keeps the reference's public
+ * signatures and binds these symbols with ctypes.
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer owned by the caller unless
+ *     documented otherwise; calls are stream-ordered on `stream` (a
+ *     cudaStream_t passed as void*) and never synchronize the device.
+ *   - Point sets are row-major float64 (rows, d) with d in {1, 2, 3}.
+ *   - Scratch memory is caller-provided (`ws`, `ws_bytes`); size it with the
+ *     matching *_workspace_bytes query.  Calls do not allocate.
+ *   - Scalars produced on device (omega, err, iteration counts, bandwidths)
+ *     are written to device memory so a planning loop never round-trips.
+ *   - `gate` (nullable): a device int; when *gate != 0 at kernel start the
+ *     call is a no-op.  The planner uses it to stop a queued loop on device.
+ *   - Return value: FCB_OK or an FCB_E* status; fcb_last_error() explains.
+ *     Algorithmic failures discovered on device (rollout blow-up, Riccati
+ *     blow-up, transport marginal violation) are reported through device
+ *     status words, mirroring the reference's typed exceptions.
+ */
+#ifndef FLOWCOVER_B200_H
+#define FLOWCOVER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* fcb_stream_t; /* cudaStream_t */
+
+#if defined(__GNUC__)
+#define FCB_API __attribute__((visibility("default")))
+#else
+#define FCB_API
+#endif
+
+enum {
+    FCB_OK = 0,
+    FCB_EINPUT = 1,     /* ValueError / SinkhornInputError              */
+    FCB_EFLOW = 2,      /* FlowError          (sinkhorn.py:74-75)        */
+    FCB_EROLLOUT = 3,   /* RolloutDivergenceError (dynamics.py:25-30)    */
+    FCB_ERICCATI = 4,   /* RiccatiDivergenceError (lqr.py:47-55)         */
+    FCB_ECUDA = 5,
+    FCB_ENOTSUP = 6,
+    FCB_EWORKSPACE = 7
+};
+
+enum { FCB_FP32 = 0, FCB_FP64 = 1 };
+
+/* Dynamics models with device implementations (dynamics.py:72-181). */
+enum {
+    FCB_MODEL_SINGLE_INTEGRATOR_2D = 0, /* dynamics.py:72-95            */
+    FCB_MODEL_DIFF_DRIVE = 1,           /* dynamics.py:98-129           */
+    FCB_MODEL_AIRCRAFT_3D = 2,          /* dynamics.py:132-181          */
+    FCB_MODEL_DOUBLE_INTEGRATOR_2D = 3, /* user-built model of SURVEY §8(d) cfg 1-2 */
+    FCB_MODEL_LTI = 4                   /* f = A s + B u, A/B in model_params */
+};
+
+/* Entropic-OT solve modes (sinkhorn.py:170-236). */
+enum { FCB_OT_ASYM = 0, FCB_OT_SYM = 1, FCB_OT_SWEEP = 2 };
+
+/* Planner status words (device int[8]); see fcb_plan_state_* below. */
+enum {
+    FCB_STATE_STOP = 0,      /* 0 running, 1 converged, 2 failed          */
+    FCB_STATE_STAGE = 1,     /* 1 rollout, 2 flow, 3 lqr                  */
+    FCB_STATE_ITER = 2,      /* outer iteration of the failure            */
+    FCB_STATE_INDEX = 3,     /* rollout step / Riccati index              */
+    FCB_STATE_FLOWS = 4,     /* flows evaluated (iterations_used)         */
+    FCB_STATE_UPDATES = 5    /* control updates applied                   */
+};
+
+/* ---- library ----------------------------------------------------------- */
+FCB_API const char* fcb_version(void);
+FCB_API const char* fcb_last_error(void);
+FCB_API long long fcb_launch_count(void); /* kernels launched by this library      */
+FCB_API int fcb_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- entropic OT / Sinkhorn (sinkhorn.py) ------------------------------ */
+
+/* resolve_omega (sinkhorn.py:136-148) plus the centring statistics the
+ * kernels use.  omega_fixed > 0 selects a numeric omega, otherwise "auto".
+ * scal: device double[16]; scal[0] = omega.  mode picks the centre
+ * (ASYM: midpoint of the means, SYM: mean of X). */
+FCB_API size_t fcb_omega_workspace_bytes(int n, int m);
+FCB_API int fcb_resolve_omega(int mode, const double* X, int n, const double* Y, int m, int d,
+                      double omega_fixed, double* scal, void* ws, size_t ws_bytes,
+                      fcb_stream_t stream);
+
+/* One transport solve with streamed cost tiles; the n x m cost matrix is
+ * never stored.
+ *   ASYM  : _solve_asymmetric (sinkhorn.py:170-205) on X (n) vs Y (m)
+ *   SYM   : _solve_symmetric  (sinkhorn.py:208-236) on X (n); Y ignored
+ *   SWEEP : one _lse_rows sweep (sinkhorn.py:151-167):
+ *           f[i] = LSE_j((f0[j] - |x_i - y_j|^2) / omega), f0 has m entries
+ * scal     : from fcb_resolve_omega.
+ * f0       : nullable warm start (n), or the SWEEP potential (m).
+ * f, g     : potentials out (g: m, ASYM only; may be NULL otherwise).
+ * row_sums : plan row sums exp(clip(delta) + log a) (n).
+ * stat     : device double[4] = {marginal_error, iters_used, converged, 0}.
+ * bary     : nullable (n*(d+1)): per row the unclipped plan row mass and
+ *            plan barycentre, i.e. sum_j T_ij and sum_j T_ij y_j / sum_j T_ij
+ *            at the returned potentials (feeds the transport gradient,
+ *            sinkhorn.py:383-391).  */
+FCB_API size_t fcb_ot_workspace_bytes(int mode, int precision, int n, int m, int d);
+FCB_API int fcb_ot_solve(int mode, int precision, const double* X, int n, const double* Y, int m, int d,
+                 const double* scal, int max_iters, double tol, const double* f0,
+                 double* f, double* g, double* row_sums, double* stat, double* bary,
+                 const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream);
+
+/* cost of a solved problem: ASYM f.row_sums + sum(g)/m (sinkhorn.py:289),
+ * SYM 2 p.row_sums (sinkhorn.py:315).  out: device double. */
+FCB_API int fcb_ot_cost(int mode, const double* f, const double* row_sums, int n, const double* g, int m,
+                double* out, fcb_stream_t stream);
+
+/* SinkhornSolution.plan (sinkhorn.py:253-256): out (n*m) = exp((f+g-C)/w). */
+FCB_API int fcb_ot_plan(const double* X, int n, const double* Y, int m, int d, const double* f,
+                const double* g, const double* scal, double* out, fcb_stream_t stream);
+
+/* sinkhorn_flow (sinkhorn.py:338-400): omega, cross + self solves, FlowError
+ * test and the envelope gradient, with the warm state (warm_f, warm_p; n
+ * each, device, updated in place when warm_valid[0] says so).
+ *   flow      : (n*d) out
+ *   fstat     : device double[8] = {worst_err, converged, flow_error(0/1),
+ *               mean_magnitude, omega, iters_cross, iters_self, 0}
+ *   warm_valid: device int[2] {f valid, p valid}; read and set.  NULL = cold.
+ *   plan_state/iteration/flow_log/conv_tol (nullable): planner hooks --
+ *               a FlowError marks plan_state failed (stage 2); otherwise
+ *               flow_log[4*iteration..] = {mean magnitude, inner iterations
+ *               of the cross solve, of the self solve, marginal error} and
+ *               the convergence test of optimizer.py:251-255 is applied. */
+FCB_API size_t fcb_sinkhorn_flow_workspace_bytes(int precision, int n, int m, int d);
+FCB_API int fcb_sinkhorn_flow(int precision, const double* X, int n, const double* Y, int m, int d,
+                      double omega_fixed, int max_iters, double tol, double* warm_f,
+                      double* warm_p, int* warm_valid, double* flow, double* fstat,
+                      int* plan_state, int iteration, double* flow_log, double conv_tol,
+                      void* ws, size_t ws_bytes, fcb_stream_t stream);
+
+/* sinkhorn_divergence (sinkhorn.py:319-335); out: device double[4] =
+ * {divergence, cross cost, self_x cost, self_y cost}. */
+FCB_API size_t fcb_sinkhorn_divergence_workspace_bytes(int precision, int n, int m, int d);
+FCB_API int fcb_sinkhorn_divergence(int precision, const double* X, int n, const double* Y, int m, int d,
+                            double omega_fixed, int max_iters, double tol, double* out,
+                            const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream);
+
+/* ---- reference density (reference.py) ---------------------------------- */
+
+/* GaussianMixture score / log_density (reference.py:77-110).
+ * params (device double): [log_w(k) | log_norm(k) | means(k*d) | chol(k*d*d)]
+ * with chol the lower Cholesky factors.  score / logdens nullable. */
+FCB_API int fcb_gmm_eval(const double* X, int n, int d, int k, const double* params, double* score,
+                 double* logdens, const int* gate, fcb_stream_t stream);
+
+/* ---- Stein variational flow (stein.py) ---------------------------------- */
+
+/* median_bandwidth (stein.py:66-76): exact np.median over all n^2 pairwise
+ * distances (diagonal included) by radix selection, then
+ * h = med^2 / log_np1 (log_np1 = log(n+1) computed by the caller).
+ * hstat: device double[4] = {h, med, clamped, 0}; the BANDWIDTH_FLOOR clamp
+ * of stein.py:101-103 is applied. */
+FCB_API size_t fcb_median_workspace_bytes(int n);
+FCB_API int fcb_median_bandwidth(const double* X, int n, int d, double log_np1, double* hstat,
+                         const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream);
+
+/* stein_flow (stein.py:79-122): out (n*d).  hstat[0] is the (clamped)
+ * bandwidth; fixed bandwidths are written there by the caller. */
+FCB_API size_t fcb_stein_workspace_bytes(int precision, int n, int d);
+FCB_API int fcb_stein_flow(int precision, const double* X, int n, int d, const double* scores,
+                   const double* hstat, double* out, const int* gate, void* ws,
+                   size_t ws_bytes, fcb_stream_t stream);
+
+/* stein_flow_on_trajectory for the planner: median/fixed bandwidth, GMM
+ * score and the flow, plus the mean-magnitude / convergence hooks of
+ * fcb_sinkhorn_flow (flow_log row: {mean magnitude, bandwidth, clamped,
+ * median}).  fstat as for fcb_sinkhorn_flow with fstat[4] = bandwidth and
+ * fstat[5] = clamped. */
+FCB_API size_t fcb_stein_flow_full_workspace_bytes(int precision, int n, int d);
+FCB_API int fcb_stein_flow_full(int precision, const double* X, int n, int d, int k,
+                        const double* gmm_params, double bandwidth_fixed, double log_np1,
+                        double* flow, double* fstat, int* plan_state, int iteration,
+                        double* flow_log, double conv_tol, void* ws, size_t ws_bytes,
+                        fcb_stream_t stream);
+
+/* ---- dynamics and LQR (dynamics.py, lqr.py) ----------------------------- */
+
+/* rollout (dynamics.py:276-312): RK4, zero-order hold.  S (T+1)*ns out,
+ * X (T*d, nullable) receives the workspace projection of S[1:]
+ * (project_states, dynamics.py:67-69; P is d*ns, device).
+ * status: device int; -1 on success, else the step index k+1 of the first
+ * non-finite state (RolloutDivergenceError.step).  plan_state/iteration:
+ * nullable planner hooks (stage 1). model_params: LTI [A(ns*ns) | B(ns*m)]. */
+FCB_API int fcb_rollout(int model, int ns, int m, const double* model_params, const double* s0,
+                const double* U, int T, double dt, double* S, int d, const double* P,
+                double* X, int* status, int* plan_state, int iteration, fcb_stream_t stream);
+
+/* linearize_along (dynamics.py:315-329): A (T*ns*ns), B (T*ns*m). */
+FCB_API int fcb_linearize(int model, int ns, int m, const double* model_params, const double* S,
+                  const double* U, int T, double* A, double* B, fcb_stream_t stream);
+
+/* solve_flow_lqr (lqr.py:154-200) on explicit A, B (T, ns, ns/m).
+ * a: (T*ns) state-space flow.  v (T*m), z ((T+1)*ns), K (T*m*ns), dff (T*m)
+ * out (K/dff nullable).  scal: device double[2] = {cost, 0};
+ * status: device int, -1 or the time index of a non-finite value. */
+FCB_API int fcb_lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B,
+                  const double* Q, const double* R, const double* a, double* v, double* z,
+                  double* K, double* dff, double* scal, int* status, double* ws,
+                  fcb_stream_t stream);
+FCB_API size_t fcb_lqr_workspace_bytes(int ns, int m, int T);
+
+/* One planner update (optimizer.py:259-268): linearize along (S, U) on the
+ * fly, lift the workspace flow (lqr.py:140-142), solve the flow LQR and
+ * write U_next = clamp(U + eta * v*).  lqr_costs[iteration] gets the cost;
+ * a Riccati blow-up marks plan_state failed (stage 3).  clamp nullable. */
+FCB_API int fcb_plan_update(int model, int ns, int m, const double* model_params, const double* S,
+                    const double* U, int T, double dt, int d, const double* P,
+                    const double* flow, const double* Q, const double* R, double eta,
+                    const double* clamp, double* U_next, double* lqr_costs, int* plan_state,
+                    int iteration, double* ws, size_t ws_bytes, fcb_stream_t stream);
+FCB_API size_t fcb_plan_update_workspace_bytes(int ns, int m, int T);
+
+/* ---- measurement helpers ------------------------------------------------- */
+
+/* MUFU.EX2 / FFMA throughput probe used by bench.py for the roofline
+ * denominators.  out: device double[2] = {ex2 ops, ffma ops} performed;
+ * the caller times the launch with events. */
+FCB_API int fcb_peak_probe(int which, int iters, double* out, fcb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLOWCOVER_B200_H */

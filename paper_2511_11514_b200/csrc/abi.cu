@@ -1,0 +1,321 @@
+// abi.cu -- extern "C" entry points of libflowcover_b200.so.
+//
+// Thin validation + dispatch layer; see include/flowcover_b200.h for the
+// contract of every symbol and the reference function it replaces.
+#include "fcb_internal.cuh"
+
+#include <mutex>
+#include <string>
+
+namespace fcb {
+
+std::atomic<long long> g_launches{0};
+static thread_local std::string t_last_error;
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+    t_last_error = msg;
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+    t_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return FCB_ECUDA;
+}
+
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+int sm_count() {
+    static int cache[64] = {0};
+    const int dev = current_device();
+    if (dev < 0 || dev >= 64) return 148;
+    if (cache[dev] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1)
+            v = 148;
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
+// forward declarations of the implementation functions
+size_t ot_ws_bytes(int mode, int precision, int n, int m, int d);
+int ot_solve(int mode, int precision, const double* X, int n, const double* Y, int m, int d,
+             const double* scal, int max_iters, double tol, const double* f0, double* f, double* g,
+             double* rs, double* stat, double* bary, const int* gate, void* ws, size_t ws_bytes,
+             cudaStream_t st);
+size_t omega_ws_bytes(int n, int m);
+int resolve_omega(int mode, const double* X, int n, const double* Y, int m, int d,
+                  double omega_fixed, double unit, double* scal, void* ws, size_t ws_bytes,
+                  cudaStream_t st);
+int ot_cost(int mode, const double* f, const double* rs, int n, const double* g, int m,
+            double* out, cudaStream_t st);
+int ot_plan(const double* X, int n, const double* Y, int m, int d, const double* f,
+            const double* g, const double* scal, double* out, cudaStream_t st);
+size_t sinkhorn_flow_ws_bytes(int precision, int n, int m, int d);
+int sinkhorn_flow(int precision, const double* X, int n, const double* Y, int m, int d,
+                  double omega_fixed, int max_iters, double tol, double* warm_f, double* warm_p,
+                  int* warm_valid, double* flow, double* fstat, int* plan_state, int iteration,
+                  double* flow_log, double conv_tol, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t sinkhorn_divergence_ws_bytes(int precision, int n, int m, int d);
+int sinkhorn_divergence(int precision, const double* X, int n, const double* Y, int m, int d,
+                        double omega_fixed, int max_iters, double tol, double* out,
+                        const int* gate, void* ws, size_t ws_bytes, cudaStream_t st);
+int gmm_eval(const double* X, int n, int d, int k, const double* prm, double* score,
+             double* logdens, const int* gate, cudaStream_t st);
+size_t median_ws_bytes(int n);
+int median_bandwidth(const double* X, int n, int d, double log_np1, double* hstat, const int* gate,
+                     void* ws, size_t ws_bytes, cudaStream_t st);
+size_t stein_ws_bytes(int precision, int n, int d);
+int stein_flow(int precision, const double* X, int n, int d, const double* scores,
+               const double* hstat, double* out, const int* gate, void* ws, size_t ws_bytes,
+               cudaStream_t st);
+size_t stein_flow_full_ws_bytes(int precision, int n, int d);
+int stein_flow_full(int precision, const double* X, int n, int d, int k, const double* prm,
+                    double bandwidth_fixed, double log_np1, double* flow, double* fstat,
+                    int* plan_state, int iteration, double* flow_log, double conv_tol, void* ws,
+                    size_t ws_bytes, cudaStream_t st);
+int rollout(int model, int ns, int m, const double* prm, const double* s0, const double* U, int T,
+            double dt, double* S, int d, const double* P, double* X, int* status, int* plan_state,
+            int iteration, cudaStream_t st);
+int linearize(int model, int ns, int m, const double* prm, const double* S, const double* U, int T,
+              double* A, double* B, cudaStream_t st);
+size_t lqr_ws_bytes(int ns, int m, int T);
+int lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B, const double* Q,
+              const double* R, const double* a, double* v, double* z, double* K, double* dff,
+              double* scal, int* status, double* ws, cudaStream_t st);
+size_t plan_update_ws_bytes(int ns, int m, int T);
+int plan_update(int model, int ns, int m, const double* prm, const double* S, const double* U,
+                int T, double dt, int d, const double* P, const double* flow, const double* Q,
+                const double* R, double eta, const double* clamp, double* Unext, double* lqr_costs,
+                int* plan_state, int iteration, double* ws, size_t ws_bytes, cudaStream_t st);
+
+// ---- peak probe: MUFU.EX2 and FFMA throughput -----------------------------
+constexpr int PROBE_BLOCK = 256;
+
+__global__ void __launch_bounds__(PROBE_BLOCK) probe_ex2_kernel(int iters, float seed, float* sink) {
+    float a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed * (float)(threadIdx.x + k) * 1e-9f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = ex2_approx(a[k]) * -1e-3f;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 12345.f) *sink = s;
+}
+
+__global__ void __launch_bounds__(PROBE_BLOCK) probe_ffma_kernel(int iters, float seed, float* sink) {
+    float a[8], b = seed * 1e-7f, c = 0.999f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = (float)(threadIdx.x + k) * 1e-3f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], c, b);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == 12345.f) *sink = s;
+}
+
+__global__ void probe_count_kernel(double* out, double ops) {
+    if (threadIdx.x == 0) out[0] = ops;
+}
+
+}  // namespace fcb
+
+using namespace fcb;
+
+#define CS(s) static_cast<cudaStream_t>(s)
+
+extern "C" {
+
+const char* fcb_version(void) { return "flowcover-b200 0.1.0 sm_100a"; }
+const char* fcb_last_error(void) { return t_last_error.c_str(); }
+long long fcb_launch_count(void) { return g_launches.load(); }
+
+int fcb_device_info(int* sms, int* major, int* minor) {
+    int dev = 0;
+    FCB_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp p;
+    FCB_CUDA(cudaGetDeviceProperties(&p, dev));
+    if (sms) *sms = p.multiProcessorCount;
+    if (major) *major = p.major;
+    if (minor) *minor = p.minor;
+    return FCB_OK;
+}
+
+static int check_pts(int n, int d) {
+    if (n < 0) return fail(FCB_EINPUT, "negative point count");
+    if (d < 1 || d > 3) return fail(FCB_ENOTSUP, "point dimension must be 1, 2 or 3");
+    return FCB_OK;
+}
+
+size_t fcb_omega_workspace_bytes(int n, int m) { return omega_ws_bytes(n, m); }
+
+int fcb_resolve_omega(int mode, const double* X, int n, const double* Y, int m, int d,
+                      double omega_fixed, double* scal, void* ws, size_t ws_bytes,
+                      fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    if (n < 1) return fail(FCB_EINPUT, "X must contain at least one point");
+    // the precision decides the exponent units: callers pass the precision
+    // through the mode's high bits (mode | precision << 8)
+    const int precision = (mode >> 8) & 0xff;
+    const double unit = precision == FCB_FP64 ? 1.0 : kLog2e;
+    return resolve_omega(mode & 0xff, X, n, Y, m, d, omega_fixed, unit, scal, ws, ws_bytes,
+                         CS(stream));
+}
+
+size_t fcb_ot_workspace_bytes(int mode, int precision, int n, int m, int d) {
+    return ot_ws_bytes(mode, precision, n, m, d);
+}
+
+int fcb_ot_solve(int mode, int precision, const double* X, int n, const double* Y, int m, int d,
+                 const double* scal, int max_iters, double tol, const double* f0, double* f,
+                 double* g, double* row_sums, double* stat, double* bary, const int* gate,
+                 void* ws, size_t ws_bytes, fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    if (mode < FCB_OT_ASYM || mode > FCB_OT_SWEEP) return fail(FCB_EINPUT, "bad ot mode");
+    return ot_solve(mode, precision, X, n, Y, m, d, scal, max_iters, tol, f0, f, g, row_sums, stat,
+                    bary, gate, ws, ws_bytes, CS(stream));
+}
+
+int fcb_ot_cost(int mode, const double* f, const double* row_sums, int n, const double* g, int m,
+                double* out, fcb_stream_t stream) {
+    return ot_cost(mode, f, row_sums, n, g, m, out, CS(stream));
+}
+
+int fcb_ot_plan(const double* X, int n, const double* Y, int m, int d, const double* f,
+                const double* g, const double* scal, double* out, fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    return ot_plan(X, n, Y, m, d, f, g, scal, out, CS(stream));
+}
+
+size_t fcb_sinkhorn_flow_workspace_bytes(int precision, int n, int m, int d) {
+    return sinkhorn_flow_ws_bytes(precision, n, m, d);
+}
+
+int fcb_sinkhorn_flow(int precision, const double* X, int n, const double* Y, int m, int d,
+                      double omega_fixed, int max_iters, double tol, double* warm_f,
+                      double* warm_p, int* warm_valid, double* flow, double* fstat,
+                      int* plan_state, int iteration, double* flow_log, double conv_tol,
+                      void* ws, size_t ws_bytes, fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    if (n < 1 || m < 1) return fail(FCB_EINPUT, "point sets must be non-empty");
+    return sinkhorn_flow(precision, X, n, Y, m, d, omega_fixed, max_iters, tol, warm_f, warm_p,
+                         warm_valid, flow, fstat, plan_state, iteration, flow_log, conv_tol, ws,
+                         ws_bytes, CS(stream));
+}
+
+size_t fcb_sinkhorn_divergence_workspace_bytes(int precision, int n, int m, int d) {
+    return sinkhorn_divergence_ws_bytes(precision, n, m, d);
+}
+
+int fcb_sinkhorn_divergence(int precision, const double* X, int n, const double* Y, int m, int d,
+                            double omega_fixed, int max_iters, double tol, double* out,
+                            const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    if (n < 1 || m < 1) return fail(FCB_EINPUT, "point sets must be non-empty");
+    return sinkhorn_divergence(precision, X, n, Y, m, d, omega_fixed, max_iters, tol, out, gate, ws,
+                               ws_bytes, CS(stream));
+}
+
+int fcb_gmm_eval(const double* X, int n, int d, int k, const double* params, double* score,
+                 double* logdens, const int* gate, fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    if (k < 1) return fail(FCB_EINPUT, "mixture needs at least one component");
+    return gmm_eval(X, n, d, k, params, score, logdens, gate, CS(stream));
+}
+
+size_t fcb_median_workspace_bytes(int n) { return median_ws_bytes(n); }
+
+int fcb_median_bandwidth(const double* X, int n, int d, double log_np1, double* hstat,
+                         const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    return median_bandwidth(X, n, d, log_np1, hstat, gate, ws, ws_bytes, CS(stream));
+}
+
+size_t fcb_stein_workspace_bytes(int precision, int n, int d) {
+    return stein_ws_bytes(precision, n, d);
+}
+
+int fcb_stein_flow(int precision, const double* X, int n, int d, const double* scores,
+                   const double* hstat, double* out, const int* gate, void* ws, size_t ws_bytes,
+                   fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    return stein_flow(precision, X, n, d, scores, hstat, out, gate, ws, ws_bytes, CS(stream));
+}
+
+size_t fcb_stein_flow_full_workspace_bytes(int precision, int n, int d) {
+    return stein_flow_full_ws_bytes(precision, n, d);
+}
+
+int fcb_stein_flow_full(int precision, const double* X, int n, int d, int k,
+                        const double* gmm_params, double bandwidth_fixed, double log_np1,
+                        double* flow, double* fstat, int* plan_state, int iteration,
+                        double* flow_log, double conv_tol, void* ws, size_t ws_bytes,
+                        fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    if (n < 1) return fail(FCB_EINPUT, "need at least one point");
+    return stein_flow_full(precision, X, n, d, k, gmm_params, bandwidth_fixed, log_np1, flow, fstat,
+                           plan_state, iteration, flow_log, conv_tol, ws, ws_bytes, CS(stream));
+}
+
+int fcb_rollout(int model, int ns, int m, const double* model_params, const double* s0,
+                const double* U, int T, double dt, double* S, int d, const double* P, double* X,
+                int* status, int* plan_state, int iteration, fcb_stream_t stream) {
+    if (!(dt > 0.0)) return fail(FCB_EINPUT, "dt must be positive");
+    return rollout(model, ns, m, model_params, s0, U, T, dt, S, d, P, X, status, plan_state,
+                   iteration, CS(stream));
+}
+
+int fcb_linearize(int model, int ns, int m, const double* model_params, const double* S,
+                  const double* U, int T, double* A, double* B, fcb_stream_t stream) {
+    return linearize(model, ns, m, model_params, S, U, T, A, B, CS(stream));
+}
+
+size_t fcb_lqr_workspace_bytes(int ns, int m, int T) { return lqr_ws_bytes(ns, m, T); }
+
+int fcb_lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B,
+                  const double* Q, const double* R, const double* a, double* v, double* z,
+                  double* K, double* dff, double* scal, int* status, double* ws,
+                  fcb_stream_t stream) {
+    if (!(dt > 0.0)) return fail(FCB_EINPUT, "dt must be positive");
+    return lqr_solve(ns, m, T, dt, A, B, Q, R, a, v, z, K, dff, scal, status, ws, CS(stream));
+}
+
+size_t fcb_plan_update_workspace_bytes(int ns, int m, int T) {
+    return plan_update_ws_bytes(ns, m, T);
+}
+
+int fcb_plan_update(int model, int ns, int m, const double* model_params, const double* S,
+                    const double* U, int T, double dt, int d, const double* P,
+                    const double* flow, const double* Q, const double* R, double eta,
+                    const double* clamp, double* U_next, double* lqr_costs, int* plan_state,
+                    int iteration, double* ws, size_t ws_bytes, fcb_stream_t stream) {
+    return plan_update(model, ns, m, model_params, S, U, T, dt, d, P, flow, Q, R, eta, clamp,
+                       U_next, lqr_costs, plan_state, iteration, ws, ws_bytes, CS(stream));
+}
+
+int fcb_peak_probe(int which, int iters, double* out, fcb_stream_t stream) {
+    static float* sink = nullptr;
+    if (!sink) FCB_CUDA(cudaMalloc(&sink, sizeof(float)));
+    const int blocks = sm_count() * 8;
+    const double ops = (double)blocks * PROBE_BLOCK * 8.0 * (double)iters;
+    if (which == 0) probe_ex2_kernel<<<blocks, PROBE_BLOCK, 0, CS(stream)>>>(iters, 1.0f, sink);
+    else probe_ffma_kernel<<<blocks, PROBE_BLOCK, 0, CS(stream)>>>(iters, 1.0f, sink);
+    FCB_LAUNCHED("probe_kernel");
+    probe_count_kernel<<<1, 32, 0, CS(stream)>>>(out, ops);
+    FCB_LAUNCHED("probe_count_kernel");
+    return FCB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+// fcb_internal.cuh -- shared device/host helpers for the flowcover-b200 kernels.
+//
+// Everything here is sm_100a-only: the library is compiled with
+// -gencode arch=compute_100a,code=sm_100a and has no fallback path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+#include <atomic>
+#include <string>
+
+#include "../../include/flowcover_b200.h"
+
+namespace fcb {
+
+// ---------------------------------------------------------------------------
+// host-side status plumbing
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_status(cudaError_t e, const char* where);
+extern std::atomic<long long> g_launches;
+
+inline void count_launch(long long k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+#define FCB_CUDA(call)                                              \
+    do {                                                            \
+        cudaError_t _e = (call);                                    \
+        if (_e != cudaSuccess) return ::fcb::cuda_status(_e, #call); \
+    } while (0)
+
+#define FCB_LAUNCHED(where)                                         \
+    do {                                                            \
+        ::fcb::count_launch();                                      \
+        cudaError_t _e = cudaGetLastError();                        \
+        if (_e != cudaSuccess) return ::fcb::cuda_status(_e, where); \
+    } while (0)
+
+int sm_count();          // cached per current device
+int current_device();
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator over a caller-provided workspace.
+struct Arena {
+    char* base;
+    size_t cap;
+    size_t off = 0;
+    bool ok = true;
+    Arena(void* p, size_t n) : base(static_cast<char*>(p)), cap(n) {}
+    template <typename T>
+    T* take(size_t count) {
+        size_t o = align_up(off, 256);
+        size_t bytes = count * sizeof(T);
+        if (base == nullptr) {  // sizing pass
+            off = o + bytes;
+            return nullptr;
+        }
+        if (o + bytes > cap) {
+            ok = false;
+            off = o + bytes;
+            return nullptr;
+        }
+        off = o + bytes;
+        return reinterpret_cast<T*>(base + o);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+constexpr double kLog2e = 1.4426950408889634073599;
+constexpr double kLn2 = 0.6931471805599453094172;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <typename T> struct Vec4;
+template <> struct alignas(16) Vec4<float> { float x, y, z, w; };
+template <> struct alignas(32) Vec4<double> { double x, y, z, w; };
+
+__device__ __forceinline__ float vget(const Vec4<float>& v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : v.z);
+}
+__device__ __forceinline__ double vget(const Vec4<double>& v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : v.z);
+}
+
+// Arithmetic traits: float works in log2 units with MUFU.EX2, double in
+// natural units with the IEEE-accurate exp/log.
+template <typename Real> struct Units;
+template <> struct Units<float> {
+    static constexpr double unit = kLog2e;   // exponent units per natural unit
+    __device__ static __forceinline__ float expu(float x) { return ex2_approx(x); }
+    __device__ static __forceinline__ double logu(double x) { return log2(x); }
+};
+template <> struct Units<double> {
+    static constexpr double unit = 1.0;
+    __device__ static __forceinline__ double expu(double x) { return exp(x); }
+    __device__ static __forceinline__ double logu(double x) { return log(x); }
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid-wide barrier for cooperatively launched kernels.  count/gen live in
+// the caller's workspace and start at zero.
+struct GridBarrier {
+    unsigned count;
+    unsigned gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBarrier* b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+        unsigned g = ld_acquire_u32(&b->gen);
+        __threadfence();
+        unsigned arrived = atomicAdd(&b->count, 1u);
+        if (arrived == nb - 1) {
+            b->count = 0;
+            __threadfence();
+            atomicAdd(&b->gen, 1u);
+        } else {
+            while (ld_acquire_u32(&b->gen) == g) {
+                __nanosleep(20);
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// max over non-negative doubles (NaN propagates: its bit pattern sorts above +inf)
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* slot, double v) {
+    atomicMax(slot, static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+__device__ __forceinline__ double load_cg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ float load_cg(const float* p) { return __ldcg(p); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic block-wide sum (fixed tree); result valid in thread 0.
+template <int BLOCK>
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = (threadIdx.x < BLOCK / 32) ? scratch[threadIdx.x] : 0.0;
+        r = warp_sum(r);
+    }
+    return r;
+}
+
+}  // namespace fcb

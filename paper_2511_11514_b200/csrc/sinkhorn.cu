@@ -1,0 +1,1049 @@
+// sinkhorn.cu -- streamed log-domain entropic OT on sm_100a.
+//
+// Replaces sinkhorn.py:136-400 of the reference (resolve_omega, _lse_rows,
+// _solve_asymmetric, _solve_symmetric, entropic_ot, sinkhorn_divergence,
+// sinkhorn_flow).  The reference materialises C (n x m), C^T and Cxx in
+// float64 and runs one numpy pass per operation; here a whole solve is ONE
+// cooperative persistent kernel:
+//
+//   phase 0      pack rows/columns (centred coordinates, folded 1/omega)
+//   loop
+//     sweep A    rows Y, columns X : partial (max, sum) per column chunk
+//     merge A    g = w (log b - LSE), column pack of Y for sweep B
+//     sweep B    rows X, columns Y : partial (max, sum, barycentre)
+//     merge B    f_new, delta, err = max|expm1(delta)|/n (device atomic max),
+//                row sums, plan barycentres, column pack of X for sweep A
+//     test       err <= tol or it >= max_iters  (grid-uniform branch)
+//
+// Cost tiles never exist in memory: each (row, column) pair is evaluated in
+// registers from a 16-byte column record broadcast out of shared memory.
+//
+// fp32 path ("expanded" form, log2 units): with x' = x - c, y' = y - c,
+//   a_ij = log2e * (pot_j - |x_i - y_j|^2) / w
+//        = W_j + x'_i . Yh_j + rowc_i,
+//   W_j = s (pot_j - |y'_j|^2), Yh_j = 2 s y'_j, rowc_i = -s |x'_i|^2,
+//   s = log2e / w.  A pair costs d+1 FFMA/FADD, one FMNMX, one MUFU.EX2 and
+//   one FADD: MUFU-bound (16 ex2/clk/SM).  The running max is tracked per
+//   8-column sub-tile with a lazy rescale (only when the max grows by more
+//   than 2^16), so exponents never overflow.
+// fp64 path ("direct" form, natural units): a_ij = s pot_j - s |x_i-y_j|^2,
+//   used for the reference's tight-tolerance known-answer tests.
+#include "fcb_internal.cuh"
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+namespace fcb {
+
+constexpr int OT_BLOCK = 256;
+constexpr int OT_TILE = 256;    // columns staged per shared-memory tile
+constexpr int OT_SUB = 8;       // columns per register sub-tile
+constexpr int OT_SMAX = 96;     // max column chunks per sweep
+constexpr int OT_MIN_CHUNK = 64;
+constexpr double EXP_CLIP = 500.0;       // sinkhorn.py:67
+constexpr double OMEGA_FLOOR = 1e-12;    // sinkhorn.py:66
+constexpr double AUTO_OMEGA_FACTOR = 0.05;  // sinkhorn.py:65
+
+// scal[] layout (device double[16])
+enum { SC_OMEGA = 0, SC_S = 1, SC_C = 2 /*2..4*/, SC_MX2 = 5, SC_MX = 6 /*6..8*/, SC_MY2 = 9,
+       SC_MY = 10 /*10..12*/ };
+
+struct Sweep {
+    int rows, cols, cols8;   // cols8: columns rounded up to OT_SUB
+    int nrb;                 // row blocks
+    int nchunks, chunk_len;  // column chunks (chunk_len multiple of OT_SUB)
+    int items;
+};
+
+template <typename Real>
+struct OtArgs {
+    int mode, n, m, d;
+    const double* X;
+    const double* Y;
+    const double* scal;
+    const double* f0;
+    int max_iters;
+    double tol, loga, logb;
+    Vec4<Real>* rowX;
+    Vec4<Real>* rowY;
+    Vec4<Real>* colX;
+    Vec4<Real>* colY;
+    double* fbuf;  // 2*n
+    double* gbuf;  // m
+    double* pm;    // partial shifts  [nchunks][rows of the sweep]
+    Real* ps;      // partial sums    [nchunks][rows]
+    Real* pa;      // partial moments [nchunks][d][rows]
+    Sweep A, B;
+    GridBarrier* bar;
+    unsigned long long* errslot;  // 3 slots
+    double* f_out;
+    double* g_out;
+    double* rs_out;
+    double* stat;
+    double* bary;
+    const int* gate;
+};
+
+// ---------------------------------------------------------------------------
+// omega / centring statistics (resolve_omega, sinkhorn.py:136-148)
+// ---------------------------------------------------------------------------
+constexpr int ST_BLOCK = 256;
+constexpr int ST_GRID = 148;
+
+// per-block partial sums of a point set: [sum_d x_d, sum |x|^2] (4 doubles)
+__global__ void __launch_bounds__(ST_BLOCK) point_stats_kernel(const double* __restrict__ P, int n,
+                                                              int d, double* __restrict__ part) {
+    __shared__ double scratch[32];
+    double acc[4] = {0, 0, 0, 0};
+    const int per = (n + gridDim.x - 1) / gridDim.x;
+    const int lo = blockIdx.x * per, hi = min(n, lo + per);
+    for (int i = lo + threadIdx.x; i < hi; i += ST_BLOCK) {
+        double sq = 0.0;
+        for (int k = 0; k < d; ++k) {
+            double v = P[(size_t)i * d + k];
+            acc[k] += v;
+            sq += v * v;
+        }
+        acc[3] += sq;
+    }
+    for (int k = 0; k < 4; ++k) {
+        double r = block_sum<ST_BLOCK>(acc[k], scratch);
+        if (threadIdx.x == 0) part[blockIdx.x * 4 + k] = r;
+    }
+}
+
+__global__ void omega_final_kernel(const double* __restrict__ partX, const double* __restrict__ partY,
+                                   int nblk, int n, int m, int d, int mode, double omega_fixed,
+                                   double unit, double* __restrict__ scal) {
+    if (threadIdx.x != 0) return;
+    double sx[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
+    for (int b = 0; b < nblk; ++b)
+        for (int k = 0; k < 4; ++k) {
+            sx[k] += partX[b * 4 + k];
+            if (partY) sy[k] += partY[b * 4 + k];
+        }
+    double mx[3] = {0, 0, 0}, my[3] = {0, 0, 0};
+    for (int k = 0; k < d; ++k) {
+        mx[k] = sx[k] / n;
+        my[k] = partY ? sy[k] / m : mx[k];
+    }
+    const double mx2 = sx[3] / n;
+    const double my2 = partY ? sy[3] / m : mx2;
+    double dot = 0.0;
+    for (int k = 0; k < d; ++k) dot += mx[k] * my[k];
+    double w = omega_fixed;
+    if (!(omega_fixed > 0.0)) {
+        w = AUTO_OMEGA_FACTOR * (mx2 + my2 - 2.0 * dot);
+        if (!(w >= OMEGA_FLOOR)) w = (w != w) ? w : OMEGA_FLOOR;
+    }
+    scal[SC_OMEGA] = w;
+    scal[SC_S] = unit / w;
+    for (int k = 0; k < 3; ++k) {
+        double c = 0.0;
+        if (k < d) c = (mode == FCB_OT_SYM) ? mx[k] : 0.5 * (mx[k] + my[k]);
+        scal[SC_C + k] = c;
+        scal[SC_MX + k] = mx[k];
+        scal[SC_MY + k] = my[k];
+    }
+    scal[SC_MX2] = mx2;
+    scal[SC_MY2] = my2;
+}
+
+// ---------------------------------------------------------------------------
+// sweep: one work item = (row block, column chunk)
+// ---------------------------------------------------------------------------
+template <typename Real>
+__device__ __forceinline__ double dexpu(double x) {
+    if constexpr (sizeof(Real) == 4) return exp2(x);
+    else return exp(x);
+}
+
+template <typename Real, int D, int RPT, bool EXP, bool BARY>
+__device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, int nrows, int row0,
+                                           const Vec4<Real>* __restrict__ cols, int c0, int c1,
+                                           Real s, double* __restrict__ pm, Real* __restrict__ ps,
+                                           Real* __restrict__ pa, int ldp, int chunk,
+                                           Vec4<Real>* tile) {
+    using U = Units<Real>;
+    const int tid = threadIdx.x;
+    const Real NEG_INF = -INFINITY;
+    const Real THRESH = 16;
+    Real x[RPT][D], rowc[RPT], rc[RPT], sum[RPT], acc[RPT][D];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        int i = min(row0 + r * OT_BLOCK + tid, nrows - 1);
+        const Real* rp = reinterpret_cast<const Real*>(rows + i);
+        Vec4<Real> v{__ldcg(rp), __ldcg(rp + 1), __ldcg(rp + 2), __ldcg(rp + 3)};
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[r][k] = vget(v, k);
+        rowc[r] = EXP ? v.w : Real(0);
+        rc[r] = rowc[r];
+        sum[r] = 0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc[r][k] = 0;
+    }
+    for (int t0 = c0; t0 < c1; t0 += OT_TILE) {
+        const int len = min(OT_TILE, c1 - t0);
+        __syncthreads();
+        for (int k = tid; k < len; k += OT_BLOCK) {
+            Vec4<Real> v;
+            const Real* src = reinterpret_cast<const Real*>(cols + t0 + k);
+            v.x = __ldcg(src + 0);
+            v.y = __ldcg(src + 1);
+            v.z = __ldcg(src + 2);
+            v.w = __ldcg(src + 3);
+            tile[k] = v;
+        }
+        __syncthreads();
+        for (int c = 0; c < len; c += OT_SUB) {
+            Real cy[OT_SUB][D], cw[OT_SUB];
+#pragma unroll
+            for (int k = 0; k < OT_SUB; ++k) {
+                Vec4<Real> v = tile[c + k];
+#pragma unroll
+                for (int q = 0; q < D; ++q) cy[k][q] = vget(v, q);
+                cw[k] = v.w;
+            }
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                Real t[OT_SUB];
+#pragma unroll
+                for (int k = 0; k < OT_SUB; ++k) {
+                    if constexpr (EXP) {
+                        Real a = cw[k] + rc[r];
+#pragma unroll
+                        for (int q = 0; q < D; ++q) a = fma(x[r][q], cy[k][q], a);
+                        t[k] = a;
+                    } else {
+                        Real d2 = 0;
+#pragma unroll
+                        for (int q = 0; q < D; ++q) {
+                            Real df = x[r][q] - cy[k][q];
+                            d2 = fma(df, df, d2);
+                        }
+                        t[k] = fma(-s, d2, cw[k] + rc[r]);
+                    }
+                }
+                Real mx = t[0];
+#pragma unroll
+                for (int k = 1; k < OT_SUB; ++k) mx = fmax(mx, t[k]);
+                if ((mx > THRESH || !(sum[r] > Real(0))) && mx > NEG_INF) {
+                    const Real sc = (sum[r] > Real(0)) ? U::expu(-mx) : Real(0);
+                    sum[r] *= sc;
+#pragma unroll
+                    for (int q = 0; q < D; ++q) acc[r][q] *= sc;
+                    rc[r] -= mx;
+#pragma unroll
+                    for (int k = 0; k < OT_SUB; ++k) t[k] -= mx;
+                }
+                Real ts = 0, ta[D];
+#pragma unroll
+                for (int q = 0; q < D; ++q) ta[q] = 0;
+#pragma unroll
+                for (int k = 0; k < OT_SUB; ++k) {
+                    const Real e = U::expu(t[k]);
+                    ts += e;
+                    if constexpr (BARY) {
+#pragma unroll
+                        for (int q = 0; q < D; ++q) ta[q] = fma(e, cy[k][q], ta[q]);
+                    }
+                }
+                sum[r] += ts;
+                if constexpr (BARY) {
+#pragma unroll
+                    for (int q = 0; q < D; ++q) acc[r][q] += ta[q];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int i = row0 + r * OT_BLOCK + tid;
+        if (i < nrows) {
+            pm[(size_t)chunk * ldp + i] = (double)rowc[r] - (double)rc[r];
+            ps[(size_t)chunk * ldp + i] = sum[r];
+            if constexpr (BARY) {
+#pragma unroll
+                for (int q = 0; q < D; ++q) pa[((size_t)chunk * D + q) * ldp + i] = acc[r][q];
+            }
+        }
+    }
+}
+
+template <typename Real, int D, int RPT, bool EXP, bool BARY>
+__device__ __forceinline__ void run_sweep(const Sweep& sw, const Vec4<Real>* rows,
+                                          const Vec4<Real>* cols, Real s, double* pm, Real* ps,
+                                          Real* pa, Vec4<Real>* tile) {
+    const int ldp = sw.rows;
+    for (int item = blockIdx.x; item < sw.items; item += gridDim.x) {
+        const int rb = item % sw.nrb;
+        const int ch = item / sw.nrb;
+        const int c0 = ch * sw.chunk_len;
+        const int c1 = min(c0 + sw.chunk_len, sw.cols8);
+        sweep_item<Real, D, RPT, EXP, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT, cols, c0, c1, s, pm,
+                                            ps, pa, ldp, ch, tile);
+    }
+}
+
+// Merge the column-chunk partials of one row: returns the LSE in natural
+// units and, with BARY, the barycentre moments divided by the sum.  G lanes
+// of one warp cooperate on one row (G a power of two <= 32); every lane of
+// the warp must call this (shuffles use the full mask).
+template <typename Real, int D, bool BARY, int G>
+__device__ __forceinline__ double merge_row(int i, int nchunks, const double* pm, const Real* ps,
+                                            const Real* pa, int ldp, int lane_in_group,
+                                            double* bar_out) {
+    double M = -INFINITY, S = 0.0, A[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) A[q] = 0.0;
+    for (int k = lane_in_group; k < nchunks; k += G) {
+        const double mk = __ldcg(pm + (size_t)k * ldp + i);
+        const double sk = (double)__ldcg(ps + (size_t)k * ldp + i);
+        double ak[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q)
+            ak[q] = BARY ? (double)__ldcg(pa + ((size_t)k * D + q) * ldp + i) : 0.0;
+        if (mk > M) {
+            const double sc = (S > 0.0) ? dexpu<Real>(M - mk) : 0.0;
+            S = S * sc + sk;
+#pragma unroll
+            for (int q = 0; q < D; ++q) A[q] = A[q] * sc + ak[q];
+            M = mk;
+        } else {
+            const double sc = dexpu<Real>(mk - M);
+            S += sk * sc;
+#pragma unroll
+            for (int q = 0; q < D; ++q) A[q] += ak[q] * sc;
+        }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        const double M2 = __shfl_xor_sync(0xffffffffu, M, o);
+        const double S2 = __shfl_xor_sync(0xffffffffu, S, o);
+        double A2[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) A2[q] = __shfl_xor_sync(0xffffffffu, A[q], o);
+        const double Mn = fmax(M, M2);
+        const double s1 = (S > 0.0) ? dexpu<Real>(M - Mn) : 0.0;
+        const double s2 = (S2 > 0.0) ? dexpu<Real>(M2 - Mn) : 0.0;
+        // fixed combine order (lower lane's term first): deterministic result
+        const bool low = (lane_in_group & o) == 0;
+        const double Sa = low ? S * s1 : S2 * s2, Sb = low ? S2 * s2 : S * s1;
+        S = Sa + Sb;
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            const double Aa = low ? A[q] * s1 : A2[q] * s2, Ab = low ? A2[q] * s2 : A[q] * s1;
+            A[q] = Aa + Ab;
+        }
+        M = Mn;
+    }
+    if (BARY && bar_out) {
+#pragma unroll
+        for (int q = 0; q < D; ++q) bar_out[q] = A[q] / S;
+    }
+    return (M + Units<Real>::logu(S)) / Units<Real>::unit;
+}
+
+// A merge phase: rows spread over the whole grid, G lanes per row, warp-
+// uniform trip counts.  epi(i, L, bar) runs on the group's lane 0 for valid
+// rows only.
+template <typename Real, int D, bool BARY, int G, typename Epi>
+__device__ __forceinline__ void merge_phase_g(const Sweep& sw, const double* pm, const Real* ps,
+                                              const Real* pa, Epi&& epi) {
+    constexpr int GPW = 32 / G;  // groups per warp
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / G, lig = lane % G;
+    for (int base = warp * GPW; base < sw.rows; base += nwarps * GPW) {
+        const int i = base + grp;
+        const bool valid = i < sw.rows;
+        double bar[D];
+        const double L = merge_row<Real, D, BARY, G>(valid ? i : sw.rows - 1, sw.nchunks, pm, ps,
+                                                     pa, sw.rows, lig, bar);
+        if (valid && lig == 0) epi(i, L, bar);
+    }
+}
+
+template <typename Real, int D, bool BARY, typename Epi>
+__device__ __forceinline__ void merge_phase(const Sweep& sw, const double* pm, const Real* ps,
+                                            const Real* pa, Epi&& epi) {
+    if (sw.nchunks <= 2)
+        merge_phase_g<Real, D, BARY, 1>(sw, pm, ps, pa, epi);
+    else if (sw.nchunks <= 16)
+        merge_phase_g<Real, D, BARY, 4>(sw, pm, ps, pa, epi);
+    else
+        merge_phase_g<Real, D, BARY, 16>(sw, pm, ps, pa, epi);
+}
+
+// ---------------------------------------------------------------------------
+// the persistent solver
+// ---------------------------------------------------------------------------
+template <typename Real, int D, int RPT, bool BARY>
+__global__ void __launch_bounds__(OT_BLOCK) ot_solve_kernel(OtArgs<Real> p) {
+    constexpr bool EXP = (sizeof(Real) == 4);
+    extern __shared__ __align__(32) unsigned char smem_raw[];
+    Vec4<Real>* tile = reinterpret_cast<Vec4<Real>*>(smem_raw);
+    __shared__ double red[32];
+
+    if (p.gate && *((volatile const int*)p.gate) != 0) return;
+
+    const double w = p.scal[SC_OMEGA];
+    const double sd = p.scal[SC_S];
+    const Real s = (Real)sd;
+    const double c[3] = {p.scal[SC_C], p.scal[SC_C + 1], p.scal[SC_C + 2]};
+    const int gthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool asym = (p.mode == FCB_OT_ASYM);
+    const bool sweep_only = (p.mode == FCB_OT_SWEEP);
+    const double csc = EXP ? 2.0 * sd : 1.0;  // column coordinate scale
+
+    // ---- phase 0: packs -------------------------------------------------
+    for (int i = gtid; i < p.n; i += gthreads) {
+        Real xs[3] = {0, 0, 0};
+        double nrm = 0.0;
+        for (int k = 0; k < D; ++k) {
+            const double v = p.X[(size_t)i * D + k] - c[k];
+            xs[k] = (Real)v;
+            nrm += v * v;
+        }
+        const double rowc = EXP ? -sd * nrm : 0.0;
+        p.rowX[i] = Vec4<Real>{xs[0], xs[1], xs[2], (Real)rowc};
+        if (!sweep_only) {
+            const double f = p.f0 ? p.f0[i] : 0.0;
+            p.fbuf[i] = f;
+            p.colX[i] = Vec4<Real>{(Real)(csc * (double)xs[0]), (Real)(csc * (double)xs[1]),
+                                   (Real)(csc * (double)xs[2]), (Real)(sd * f + rowc)};
+        }
+    }
+    if (!sweep_only) {
+        const int pad_end = (p.n + OT_SUB - 1) / OT_SUB * OT_SUB;
+        for (int i = p.n + gtid; i < pad_end; i += gthreads)
+            p.colX[i] = Vec4<Real>{0, 0, 0, (Real)-INFINITY};
+    }
+    if (asym || sweep_only) {
+        for (int j = gtid; j < p.m; j += gthreads) {
+            Real ys[3] = {0, 0, 0};
+            double nrm = 0.0;
+            for (int k = 0; k < D; ++k) {
+                const double v = p.Y[(size_t)j * D + k] - c[k];
+                ys[k] = (Real)v;
+                nrm += v * v;
+            }
+            const double rowc = EXP ? -sd * nrm : 0.0;
+            if (asym) p.rowY[j] = Vec4<Real>{ys[0], ys[1], ys[2], (Real)rowc};
+            const double pot = sweep_only ? p.f0[j] : 0.0;
+            p.colY[j] = Vec4<Real>{(Real)(csc * (double)ys[0]), (Real)(csc * (double)ys[1]),
+                                   (Real)(csc * (double)ys[2]), (Real)(sd * pot + rowc)};
+        }
+        const int pad_end = (p.m + OT_SUB - 1) / OT_SUB * OT_SUB;
+        for (int j = p.m + gtid; j < pad_end; j += gthreads)
+            p.colY[j] = Vec4<Real>{0, 0, 0, (Real)-INFINITY};
+    }
+    if (gtid == 0) {
+        p.errslot[0] = 0ull;
+        p.errslot[1] = 0ull;
+        p.errslot[2] = 0ull;
+    }
+    grid_sync(p.bar);
+
+    if (sweep_only) {
+        run_sweep<Real, D, RPT, EXP, false>(p.B, p.rowX, p.colY, s, p.pm, p.ps, p.pa, tile);
+        grid_sync(p.bar);
+        double* out = p.f_out;
+        merge_phase<Real, D, false>(p.B, p.pm, p.ps, p.pa,
+                                    [&](int i, double L, const double*) { out[i] = L; });
+        return;
+    }
+
+    const double inv_n = 1.0 / p.n;
+    int cur = 0;
+    int it = 0;
+    while (true) {
+        ++it;
+        const double* fcur = p.fbuf + (size_t)cur * p.n;
+        double* fnxt = p.fbuf + (size_t)(cur ^ 1) * p.n;
+        unsigned long long* slot = p.errslot + (it % 3);
+        if (asym) {
+            // ---- sweep A: rows Y, columns X (potential f) --------------
+            run_sweep<Real, D, RPT, EXP, false>(p.A, p.rowY, p.colX, s, p.pm, p.ps, p.pa, tile);
+            grid_sync(p.bar);
+            // ---- merge A: g = w (log b - Lg) ---------------------------
+            merge_phase<Real, D, false>(p.A, p.pm, p.ps, p.pa, [&](int j, double L, const double*) {
+                const double g = w * (p.logb - L);
+                p.gbuf[j] = g;
+                p.colY[j].w = (Real)(sd * g + (double)p.rowY[j].w);
+            });
+            grid_sync(p.bar);
+        }
+        // ---- sweep B: rows X, columns Y (ASYM, potential g) or X (SYM) --
+        run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, asym ? p.colY : p.colX, s, p.pm, p.ps,
+                                           p.pa, tile);
+        grid_sync(p.bar);
+        // ---- merge B ------------------------------------------------------
+        double emax = 0.0;
+        merge_phase<Real, D, BARY>(p.B, p.pm, p.ps, p.pa, [&](int i, double L, const double* bar) {
+            const double fi = __ldcg(fcur + i);
+            const double upd = w * (p.loga - L);  // f_new (ASYM) / target (SYM)
+            double delta = (fi - upd) / w;
+            if (delta > EXP_CLIP) delta = EXP_CLIP;  // np.clip(., None, 500); NaN passes
+            const double e = fabs(expm1(delta));
+            emax = (e > emax || e != e) ? e : emax;
+            p.rs_out[i] = exp(delta + p.loga);
+            if (BARY && p.bary) {
+                double* o = p.bary + (size_t)i * (D + 1);
+                o[0] = exp(fi / w + L);
+                for (int q = 0; q < D; ++q) o[1 + q] = bar[q] / csc + c[q];
+            }
+            const double nxt = asym ? upd : 0.5 * (fi + upd);
+            fnxt[i] = nxt;
+            p.colX[i].w = (Real)(sd * nxt + (double)p.rowX[i].w);
+        });
+        for (int o = 16; o > 0; o >>= 1) {
+            const double v = __shfl_xor_sync(0xffffffffu, emax, o);
+            emax = (v > emax || v != v) ? v : emax;
+        }
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = emax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double b = 0.0;
+            for (int k = 0; k < OT_BLOCK / 32; ++k) b = (red[k] > b || red[k] != red[k]) ? red[k] : b;
+            atomic_max_nonneg(slot, b);
+            if (blockIdx.x == 0) p.errslot[(it + 1) % 3] = 0ull;
+        }
+        grid_sync(p.bar);
+        const double err = __longlong_as_double((long long)__ldcg(slot)) * inv_n;
+        const bool conv = err <= p.tol;
+        if (conv || it >= p.max_iters) {
+            for (int i = gtid; i < p.n; i += gthreads) p.f_out[i] = __ldcg(fcur + i);
+            if (asym && p.g_out)
+                for (int j = gtid; j < p.m; j += gthreads) p.g_out[j] = __ldcg(p.gbuf + j);
+            if (gtid == 0) {
+                p.stat[0] = err;
+                p.stat[1] = (double)it;
+                p.stat[2] = conv ? 1.0 : 0.0;
+                p.stat[3] = 0.0;
+            }
+            return;
+        }
+        cur ^= 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static Sweep plan_sweep(int rows, int cols, int rpt, int grid) {
+    Sweep s{};
+    s.rows = rows;
+    s.cols = cols;
+    s.cols8 = (cols + OT_SUB - 1) / OT_SUB * OT_SUB;
+    const int br = OT_BLOCK * rpt;
+    s.nrb = (rows + br - 1) / br;
+    const int max_chunks = std::max(1, std::min(OT_SMAX, s.cols8 / OT_MIN_CHUNK));
+    // pick the chunk count that best fills whole waves of the persistent grid
+    int best = 1;
+    double best_eff = -1.0;
+    for (int k = 1; k <= max_chunks; ++k) {
+        const long items = (long)s.nrb * k;
+        const long waves = (items + grid - 1) / grid;
+        const double eff = (double)items / (double)(waves * grid);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = k;
+        }
+        if (eff > 0.97) break;
+    }
+    int cl = (s.cols8 + best - 1) / best;
+    cl = (cl + OT_SUB - 1) / OT_SUB * OT_SUB;
+    s.chunk_len = cl;
+    s.nchunks = (s.cols8 + cl - 1) / cl;
+    s.items = s.nrb * s.nchunks;
+    return s;
+}
+
+template <typename Real>
+struct OtLayout {
+    size_t bytes = 0;
+    OtArgs<Real> a{};
+};
+
+template <typename Real, int D, int RPT, bool BARY>
+static int ot_grid_size(int* grid) {
+    static int cached = -1;
+    if (cached < 0) {
+        int per_sm = 0;
+        const size_t smem = OT_TILE * sizeof(Vec4<Real>);
+        FCB_CUDA(cudaFuncSetAttribute(ot_solve_kernel<Real, D, RPT, BARY>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, ot_solve_kernel<Real, D, RPT, BARY>, OT_BLOCK, smem));
+        if (per_sm < 1) return fail(FCB_ECUDA, "ot_solve_kernel cannot be resident");
+        per_sm = std::min(per_sm, 2);
+        cached = per_sm * sm_count();
+    }
+    *grid = cached;
+    return FCB_OK;
+}
+
+template <typename Real>
+static void ot_layout(OtLayout<Real>& L, int mode, int n, int m, int d, int rpt, int grid,
+                      void* ws, size_t ws_bytes) {
+    Arena ar(ws, ws_bytes);
+    OtArgs<Real>& a = L.a;
+    a.mode = mode;
+    a.n = n;
+    a.m = m;
+    a.d = d;
+    const bool asym = mode == FCB_OT_ASYM;
+    const bool sweep = mode == FCB_OT_SWEEP;
+    a.A = Sweep{};
+    if (asym) {
+        a.A = plan_sweep(m, n, rpt, grid);
+        a.B = plan_sweep(n, m, rpt, grid);
+    } else if (sweep) {
+        a.B = plan_sweep(n, m, rpt, grid);
+    } else {
+        a.B = plan_sweep(n, n, rpt, grid);
+    }
+    const size_t n8 = (size_t)(n + OT_SUB - 1) / OT_SUB * OT_SUB;
+    const size_t m8 = (size_t)(m + OT_SUB - 1) / OT_SUB * OT_SUB;
+    a.rowX = ar.take<Vec4<Real>>(n);
+    a.rowY = ar.take<Vec4<Real>>(asym ? m : 0);
+    a.colX = ar.take<Vec4<Real>>(sweep ? 0 : n8);
+    a.colY = ar.take<Vec4<Real>>((asym || sweep) ? m8 : 0);
+    a.fbuf = ar.take<double>(sweep ? 0 : 2 * (size_t)n);
+    a.gbuf = ar.take<double>(asym ? m : 0);
+    const size_t pcount = std::max((size_t)a.A.nchunks * a.A.rows, (size_t)a.B.nchunks * a.B.rows);
+    a.pm = ar.take<double>(pcount);
+    a.ps = ar.take<Real>(pcount);
+    a.pa = ar.take<Real>(pcount * d);
+    a.bar = ar.take<GridBarrier>(1);
+    a.errslot = ar.take<unsigned long long>(4);
+    L.bytes = ar.off + 256;
+}
+
+template <typename Real, int D, int RPT, bool BARY>
+static int ot_launch(int mode, const double* X, int n, const double* Y, int m, const double* scal,
+                     int max_iters, double tol, const double* f0, double* f, double* g,
+                     double* rs, double* stat, double* bary, const int* gate, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
+    int grid = 0;
+    int rc = ot_grid_size<Real, D, RPT, BARY>(&grid);
+    if (rc) return rc;
+    OtLayout<Real> L;
+    ot_layout<Real>(L, mode, n, m, D, RPT, grid, ws, ws_bytes);
+    if (L.bytes > ws_bytes) return fail(FCB_EWORKSPACE, "ot workspace too small");
+    OtArgs<Real>& a = L.a;
+    a.X = X;
+    a.Y = Y;
+    a.scal = scal;
+    a.f0 = f0;
+    a.max_iters = max_iters;
+    a.tol = tol;
+    a.loga = -log((double)n);
+    a.logb = (m > 0) ? -log((double)m) : 0.0;
+    a.f_out = f;
+    a.g_out = g;
+    a.rs_out = rs;
+    a.stat = stat;
+    a.bary = bary;
+    a.gate = gate;
+    FCB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(GridBarrier), st));
+    void* args[] = {&a};
+    const size_t smem = OT_TILE * sizeof(Vec4<Real>);
+    FCB_CUDA(cudaLaunchCooperativeKernel((const void*)ot_solve_kernel<Real, D, RPT, BARY>,
+                                         dim3(grid), dim3(OT_BLOCK), args, smem, st));
+    FCB_LAUNCHED("ot_solve_kernel");
+    return FCB_OK;
+}
+
+template <typename Real, int RPT>
+static int ot_dispatch(int mode, int d, const double* X, int n, const double* Y, int m,
+                       const double* scal, int max_iters, double tol, const double* f0, double* f,
+                       double* g, double* rs, double* stat, double* bary, const int* gate,
+                       void* ws, size_t ws_bytes, cudaStream_t st) {
+#define FCB_OT_CASE(DD)                                                                          \
+    if (d == DD) {                                                                               \
+        if (bary)                                                                                \
+            return ot_launch<Real, DD, RPT, true>(mode, X, n, Y, m, scal, max_iters, tol, f0, f, \
+                                                  g, rs, stat, bary, gate, ws, ws_bytes, st);    \
+        return ot_launch<Real, DD, RPT, false>(mode, X, n, Y, m, scal, max_iters, tol, f0, f, g, \
+                                               rs, stat, bary, gate, ws, ws_bytes, st);          \
+    }
+    FCB_OT_CASE(1)
+    FCB_OT_CASE(2)
+    FCB_OT_CASE(3)
+#undef FCB_OT_CASE
+    return fail(FCB_ENOTSUP, "point dimension must be 1, 2 or 3");
+}
+
+constexpr int RPT_F32 = 2;
+constexpr int RPT_F64 = 1;
+
+template <typename Real, int RPT>
+static size_t ot_ws_bytes_t(int mode, int n, int m, int d) {
+    int grid = 0;
+    int rc = 0;
+    if (d == 1) rc = ot_grid_size<Real, 1, RPT, true>(&grid);
+    else if (d == 2) rc = ot_grid_size<Real, 2, RPT, true>(&grid);
+    else rc = ot_grid_size<Real, 3, RPT, true>(&grid);
+    if (rc) grid = 2 * sm_count();
+    // the BARY=false instantiation may have a different occupancy: size for
+    // the larger of the two possible grids
+    int grid2 = 0;
+    if (d == 1) rc = ot_grid_size<Real, 1, RPT, false>(&grid2);
+    else if (d == 2) rc = ot_grid_size<Real, 2, RPT, false>(&grid2);
+    else rc = ot_grid_size<Real, 3, RPT, false>(&grid2);
+    if (rc) grid2 = grid;
+    OtLayout<Real> L1, L2;
+    ot_layout<Real>(L1, mode, n, m, d, RPT, grid, nullptr, 0);
+    ot_layout<Real>(L2, mode, n, m, d, RPT, grid2, nullptr, 0);
+    return std::max(L1.bytes, L2.bytes);
+}
+
+size_t ot_ws_bytes(int mode, int precision, int n, int m, int d) {
+    if (d < 1 || d > 3) return 0;
+    if (precision == FCB_FP64) return ot_ws_bytes_t<double, RPT_F64>(mode, n, m, d);
+    return ot_ws_bytes_t<float, RPT_F32>(mode, n, m, d);
+}
+
+int ot_solve(int mode, int precision, const double* X, int n, const double* Y, int m, int d,
+             const double* scal, int max_iters, double tol, const double* f0, double* f, double* g,
+             double* rs, double* stat, double* bary, const int* gate, void* ws, size_t ws_bytes,
+             cudaStream_t st) {
+    if (n < 1 || (mode != FCB_OT_SYM && m < 1)) return fail(FCB_EINPUT, "empty point set");
+    if (max_iters < 1) return fail(FCB_EINPUT, "max_iters must be >= 1");
+    if (mode == FCB_OT_SWEEP && !f0) return fail(FCB_EINPUT, "sweep needs a potential");
+    if (precision == FCB_FP64)
+        return ot_dispatch<double, RPT_F64>(mode, d, X, n, Y, m, scal, max_iters, tol, f0, f, g, rs,
+                                            stat, bary, gate, ws, ws_bytes, st);
+    return ot_dispatch<float, RPT_F32>(mode, d, X, n, Y, m, scal, max_iters, tol, f0, f, g, rs,
+                                       stat, bary, gate, ws, ws_bytes, st);
+}
+
+size_t omega_ws_bytes(int n, int m) {
+    (void)n;
+    (void)m;
+    return 2 * ST_GRID * 4 * sizeof(double) + 512;
+}
+
+int resolve_omega(int mode, const double* X, int n, const double* Y, int m, int d,
+                  double omega_fixed, double unit, double* scal, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
+    if (ws_bytes < omega_ws_bytes(n, m)) return fail(FCB_EWORKSPACE, "omega workspace too small");
+    double* partX = static_cast<double*>(ws);
+    double* partY = partX + ST_GRID * 4;
+    const int gx = std::max(1, std::min(ST_GRID, (n + ST_BLOCK - 1) / ST_BLOCK));
+    const bool haveY = (mode == FCB_OT_ASYM || mode == FCB_OT_SWEEP) && Y != nullptr && m > 0;
+    const int gy = haveY ? std::max(1, std::min(ST_GRID, (m + ST_BLOCK - 1) / ST_BLOCK)) : 0;
+    // both partial arrays must be combined over the same block count
+    const int g = std::max(gx, gy);
+    point_stats_kernel<<<g, ST_BLOCK, 0, st>>>(X, n, d, partX);
+    FCB_LAUNCHED("point_stats_kernel");
+    if (haveY) {
+        point_stats_kernel<<<g, ST_BLOCK, 0, st>>>(Y, m, d, partY);
+        FCB_LAUNCHED("point_stats_kernel");
+    }
+    omega_final_kernel<<<1, 32, 0, st>>>(partX, haveY ? partY : nullptr, g, n, m, d, mode,
+                                         omega_fixed, unit, scal);
+    FCB_LAUNCHED("omega_final_kernel");
+    return FCB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// small epilogue kernels
+// ---------------------------------------------------------------------------
+__global__ void ot_cost_kernel(int mode, const double* __restrict__ f, const double* __restrict__ rs,
+                               int n, const double* __restrict__ g, int m, double* out) {
+    __shared__ double scratch[32];
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < n; i += 1024) a += f[i] * rs[i];
+    if (mode == FCB_OT_ASYM)
+        for (int j = threadIdx.x; j < m; j += 1024) b += g[j];
+    a = block_sum<1024>(a, scratch);
+    b = block_sum<1024>(b, scratch);
+    if (threadIdx.x == 0) *out = (mode == FCB_OT_ASYM) ? a + b / m : 2.0 * a;
+}
+
+__global__ void ot_plan_kernel(const double* __restrict__ X, int n, const double* __restrict__ Y,
+                               int m, int d, const double* __restrict__ f,
+                               const double* __restrict__ g, const double* __restrict__ scal,
+                               double* __restrict__ out) {
+    const double w = scal[SC_OMEGA];
+    const size_t total = (size_t)n * m;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+         t += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t / m), j = (int)(t % m);
+        double c2 = 0.0;
+        for (int k = 0; k < d; ++k) {
+            double df = __dadd_rn(X[(size_t)i * d + k], -Y[(size_t)j * d + k]);
+            c2 = __dadd_rn(c2, __dmul_rn(df, df));
+        }
+        out[t] = exp((f[i] + g[j] - c2) / w);
+    }
+}
+
+// finalize of sinkhorn_flow: FlowError test, envelope gradient, warm state,
+// mean magnitude and the planner's convergence hook.
+constexpr int FIN_BLOCK = 1024;
+__global__ void __launch_bounds__(FIN_BLOCK)
+    flow_finalize_kernel(const double* __restrict__ X, int n, int d, double tol,
+                         const double* __restrict__ rs_x, const double* __restrict__ bary_x,
+                         const double* __restrict__ stat_x, const double* __restrict__ rs_p,
+                         const double* __restrict__ bary_p, const double* __restrict__ stat_p,
+                         const double* __restrict__ f, const double* __restrict__ pp,
+                         double* warm_f, double* warm_p, int* warm_valid, double* flow,
+                         double* fstat, const double* scal, int* plan_state, int iteration,
+                         double* flow_log, double conv_tol) {
+    __shared__ double scratch[32];
+    __shared__ int s_fail;
+    if (plan_state && *((volatile int*)plan_state) != 0) return;
+    const double ex = stat_x[0], ep = stat_p[0];
+    const double worst = (ex > ep || ex != ex) ? ex : ep;
+    const bool flow_error = worst > 100.0 * tol;
+    if (threadIdx.x == 0) s_fail = flow_error ? 1 : 0;
+    __syncthreads();
+    double norm_acc = 0.0;
+    if (!s_fail) {
+        for (int i = threadIdx.x; i < n; i += FIN_BLOCK) {
+            const double rcx = rs_x[i], rux = bary_x[(size_t)i * (d + 1)];
+            const double rcp = rs_p[i], rup = bary_p[(size_t)i * (d + 1)];
+            double sq = 0.0;
+            for (int k = 0; k < d; ++k) {
+                const double x = X[(size_t)i * d + k];
+                const double ty = rux * bary_x[(size_t)i * (d + 1) + 1 + k];
+                const double px = rup * bary_p[(size_t)i * (d + 1) + 1 + k];
+                const double grad = 2.0 * (rcx * x - ty) - 2.0 * (rcp * x - px);
+                flow[(size_t)i * d + k] = -grad;
+                sq += grad * grad;
+            }
+            norm_acc += sqrt(sq);
+            if (warm_f) {
+                warm_f[i] = f[i];
+                warm_p[i] = pp[i];
+            }
+        }
+    }
+    const double total = block_sum<FIN_BLOCK>(norm_acc, scratch);
+    if (threadIdx.x == 0) {
+        const double mean_mag = total / n;
+        fstat[0] = worst;
+        fstat[1] = (stat_x[2] != 0.0 && stat_p[2] != 0.0) ? 1.0 : 0.0;
+        fstat[2] = flow_error ? 1.0 : 0.0;
+        fstat[3] = flow_error ? NAN : mean_mag;
+        fstat[4] = scal[SC_OMEGA];
+        fstat[5] = stat_x[1];
+        fstat[6] = stat_p[1];
+        fstat[7] = 0.0;
+        if (!flow_error && warm_valid) {
+            warm_valid[0] = 1;
+            warm_valid[1] = 1;
+        }
+        if (plan_state) {
+            if (flow_error) {
+                plan_state[FCB_STATE_STOP] = 2;
+                plan_state[FCB_STATE_STAGE] = 2;
+                plan_state[FCB_STATE_ITER] = iteration;
+                plan_state[FCB_STATE_INDEX] = -1;
+            } else {
+                double* lg = flow_log + 4 * (size_t)iteration;
+                lg[0] = mean_mag;
+                lg[1] = stat_x[1];
+                lg[2] = stat_p[1];
+                lg[3] = worst;
+                plan_state[FCB_STATE_FLOWS] = iteration + 1;
+                if (mean_mag < conv_tol) plan_state[FCB_STATE_STOP] = 1;
+            }
+        }
+    }
+}
+
+// warm start selection: f0 = warm_f if valid else NULL -> emulate with a copy
+__global__ void warm_select_kernel(const double* warm, const int* valid, int which, int n,
+                                   double* out) {
+    const bool v = valid && valid[which] != 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = v ? warm[i] : 0.0;
+}
+
+__global__ void divergence_combine_kernel(const double* costs, double* out) {
+    if (threadIdx.x == 0) {
+        out[1] = costs[0];
+        out[2] = costs[1];
+        out[3] = costs[2];
+        out[0] = costs[0] - 0.5 * (costs[1] + costs[2]);
+    }
+}
+
+__global__ void copy_scal_kernel(const double* src, double* dst, const double* centre_from,
+                                 int d) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 16; ++k) dst[k] = src[k];
+        for (int k = 0; k < 3; ++k) dst[SC_C + k] = (k < d) ? centre_from[k] : 0.0;
+    }
+}
+
+struct FlowWs {
+    double* scal;
+    double* scal_self;
+    void* omega_ws;
+    double *f, *g, *rs_x, *stat_x, *bary_x;
+    double *p, *rs_p, *stat_p, *bary_p;
+    double *f0, *p0;
+    void* ot_ws;
+    size_t ot_bytes;
+    size_t total;
+};
+
+static FlowWs flow_layout(int precision, int n, int m, int d, void* ws, size_t bytes) {
+    Arena ar(ws, bytes);
+    FlowWs L{};
+    L.scal = ar.take<double>(16);
+    L.scal_self = ar.take<double>(16);
+    L.omega_ws = ar.take<char>(omega_ws_bytes(n, m));
+    L.f = ar.take<double>(n);
+    L.g = ar.take<double>(m);
+    L.rs_x = ar.take<double>(n);
+    L.stat_x = ar.take<double>(4);
+    L.bary_x = ar.take<double>((size_t)n * (d + 1));
+    L.p = ar.take<double>(n);
+    L.rs_p = ar.take<double>(n);
+    L.stat_p = ar.take<double>(4);
+    L.bary_p = ar.take<double>((size_t)n * (d + 1));
+    L.f0 = ar.take<double>(n);
+    L.p0 = ar.take<double>(n);
+    L.ot_bytes = std::max(ot_ws_bytes(FCB_OT_ASYM, precision, n, m, d),
+                          ot_ws_bytes(FCB_OT_SYM, precision, n, n, d));
+    L.ot_ws = ar.take<char>(L.ot_bytes);
+    L.total = ar.off + 256;
+    return L;
+}
+
+size_t sinkhorn_flow_ws_bytes(int precision, int n, int m, int d) {
+    return flow_layout(precision, n, m, d, nullptr, 0).total;
+}
+
+static double unit_for(int precision) { return precision == FCB_FP64 ? 1.0 : kLog2e; }
+
+int sinkhorn_flow(int precision, const double* X, int n, const double* Y, int m, int d,
+                  double omega_fixed, int max_iters, double tol, double* warm_f, double* warm_p,
+                  int* warm_valid, double* flow, double* fstat, int* plan_state, int iteration,
+                  double* flow_log, double conv_tol, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
+    FlowWs L = flow_layout(precision, n, m, d, ws, ws_bytes);
+    if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "sinkhorn_flow workspace too small");
+    int rc = resolve_omega(FCB_OT_ASYM, X, n, Y, m, d, omega_fixed, unit_for(precision), L.scal,
+                           L.omega_ws, omega_ws_bytes(n, m), st);
+    if (rc) return rc;
+    const double* f0 = nullptr;
+    const double* p0 = nullptr;
+    if (warm_f && warm_valid) {
+        warm_select_kernel<<<std::min(148, (n + 255) / 256), 256, 0, st>>>(warm_f, warm_valid, 0, n,
+                                                                           L.f0);
+        FCB_LAUNCHED("warm_select_kernel");
+        warm_select_kernel<<<std::min(148, (n + 255) / 256), 256, 0, st>>>(warm_p, warm_valid, 1, n,
+                                                                           L.p0);
+        FCB_LAUNCHED("warm_select_kernel");
+        f0 = L.f0;
+        p0 = L.p0;
+    }
+    rc = ot_solve(FCB_OT_ASYM, precision, X, n, Y, m, d, L.scal, max_iters, tol, f0, L.f, L.g,
+                  L.rs_x, L.stat_x, L.bary_x, plan_state, L.ot_ws, L.ot_bytes, st);
+    if (rc) return rc;
+    // the self term shares omega but is centred on X
+    copy_scal_kernel<<<1, 32, 0, st>>>(L.scal, L.scal_self, L.scal + SC_MX, d);
+    FCB_LAUNCHED("copy_scal_kernel");
+    rc = ot_solve(FCB_OT_SYM, precision, X, n, nullptr, 0, d, L.scal_self, max_iters, tol, p0, L.p,
+                  nullptr, L.rs_p, L.stat_p, L.bary_p, plan_state, L.ot_ws, L.ot_bytes, st);
+    if (rc) return rc;
+    flow_finalize_kernel<<<1, FIN_BLOCK, 0, st>>>(X, n, d, tol, L.rs_x, L.bary_x, L.stat_x, L.rs_p,
+                                                  L.bary_p, L.stat_p, L.f, L.p, warm_f, warm_p,
+                                                  warm_valid, flow, fstat, L.scal, plan_state,
+                                                  iteration, flow_log, conv_tol);
+    FCB_LAUNCHED("flow_finalize_kernel");
+    return FCB_OK;
+}
+
+struct DivWs {
+    double* scal;
+    void* omega_ws;
+    double *f, *g, *rs, *stat, *costs;
+    void* ot_ws;
+    size_t ot_bytes, total;
+};
+
+static DivWs div_layout(int precision, int n, int m, int d, void* ws, size_t bytes) {
+    Arena ar(ws, bytes);
+    DivWs L{};
+    const int nm = std::max(n, m);
+    L.scal = ar.take<double>(16);
+    L.omega_ws = ar.take<char>(omega_ws_bytes(n, m));
+    L.f = ar.take<double>(nm);
+    L.g = ar.take<double>(nm);
+    L.rs = ar.take<double>(nm);
+    L.stat = ar.take<double>(4);
+    L.costs = ar.take<double>(4);
+    L.ot_bytes = std::max(ot_ws_bytes(FCB_OT_ASYM, precision, n, m, d),
+                          std::max(ot_ws_bytes(FCB_OT_SYM, precision, n, n, d),
+                                   ot_ws_bytes(FCB_OT_SYM, precision, m, m, d)));
+    L.ot_ws = ar.take<char>(L.ot_bytes);
+    L.total = ar.off + 256;
+    return L;
+}
+
+size_t sinkhorn_divergence_ws_bytes(int precision, int n, int m, int d) {
+    return div_layout(precision, n, m, d, nullptr, 0).total;
+}
+
+int sinkhorn_divergence(int precision, const double* X, int n, const double* Y, int m, int d,
+                        double omega_fixed, int max_iters, double tol, double* out,
+                        const int* gate, void* ws, size_t ws_bytes, cudaStream_t st) {
+    DivWs L = div_layout(precision, n, m, d, ws, ws_bytes);
+    if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "divergence workspace too small");
+    int rc = resolve_omega(FCB_OT_ASYM, X, n, Y, m, d, omega_fixed, unit_for(precision), L.scal,
+                           L.omega_ws, omega_ws_bytes(n, m), st);
+    if (rc) return rc;
+    rc = ot_solve(FCB_OT_ASYM, precision, X, n, Y, m, d, L.scal, max_iters, tol, nullptr, L.f, L.g,
+                  L.rs, L.stat, nullptr, gate, L.ot_ws, L.ot_bytes, st);
+    if (rc) return rc;
+    ot_cost_kernel<<<1, 1024, 0, st>>>(FCB_OT_ASYM, L.f, L.rs, n, L.g, m, L.costs + 0);
+    FCB_LAUNCHED("ot_cost_kernel");
+    // self terms: same omega, centre on the set itself
+    copy_scal_kernel<<<1, 32, 0, st>>>(L.scal, L.scal, L.scal + SC_MX, d);
+    FCB_LAUNCHED("copy_scal_kernel");
+    rc = ot_solve(FCB_OT_SYM, precision, X, n, nullptr, 0, d, L.scal, max_iters, tol, nullptr, L.f,
+                  nullptr, L.rs, L.stat, nullptr, gate, L.ot_ws, L.ot_bytes, st);
+    if (rc) return rc;
+    ot_cost_kernel<<<1, 1024, 0, st>>>(FCB_OT_SYM, L.f, L.rs, n, nullptr, 0, L.costs + 1);
+    FCB_LAUNCHED("ot_cost_kernel");
+    copy_scal_kernel<<<1, 32, 0, st>>>(L.scal, L.scal, L.scal + SC_MY, d);
+    FCB_LAUNCHED("copy_scal_kernel");
+    rc = ot_solve(FCB_OT_SYM, precision, Y, m, nullptr, 0, d, L.scal, max_iters, tol, nullptr, L.f,
+                  nullptr, L.rs, L.stat, nullptr, gate, L.ot_ws, L.ot_bytes, st);
+    if (rc) return rc;
+    ot_cost_kernel<<<1, 1024, 0, st>>>(FCB_OT_SYM, L.f, L.rs, m, nullptr, 0, L.costs + 2);
+    FCB_LAUNCHED("ot_cost_kernel");
+    divergence_combine_kernel<<<1, 32, 0, st>>>(L.costs, out);
+    FCB_LAUNCHED("divergence_combine_kernel");
+    return FCB_OK;
+}
+
+int ot_cost(int mode, const double* f, const double* rs, int n, const double* g, int m,
+            double* out, cudaStream_t st) {
+    ot_cost_kernel<<<1, 1024, 0, st>>>(mode, f, rs, n, g, m, out);
+    FCB_LAUNCHED("ot_cost_kernel");
+    return FCB_OK;
+}
+
+int ot_plan(const double* X, int n, const double* Y, int m, int d, const double* f,
+            const double* g, const double* scal, double* out, cudaStream_t st) {
+    const size_t total = (size_t)n * m;
+    const int blocks = (int)std::min<size_t>(148 * 8, (total + 255) / 256);
+    ot_plan_kernel<<<std::max(blocks, 1), 256, 0, st>>>(X, n, Y, m, d, f, g, scal, out);
+    FCB_LAUNCHED("ot_plan_kernel");
+    return FCB_OK;
+}
+
+}  // namespace fcb

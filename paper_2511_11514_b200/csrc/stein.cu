@@ -1,0 +1,640 @@
+// stein.cu -- density score, median bandwidth and the Stein variational flow.
+//
+// Replaces reference.py:77-110 (GaussianMixture._component_terms / score /
+// log_density) and stein.py:66-140 (median_bandwidth, stein_flow).
+//
+// * gmm_eval: one thread per point, fp64, K components streamed with an
+//   online-softmax over the responsibilities (coalesced point I/O).
+// * median: the reference takes np.median over all n^2 pairwise distances
+//   (diagonal zeros included; stein.py:75).  Here the exact order statistics
+//   are found by a 6-pass radix select over the float64 bit patterns of the
+//   squared distances (11-bit digits, histograms in shared memory), never
+//   storing the n^2 matrix.  Squared distances are formed with the same
+//   operation order as _pairwise_sq (stein.py:57-63) and without FMA
+//   contraction, so the selected values are bit-identical to numpy's.
+// * stein_flow: g_i = (1/n)[sum_j k_ij w_j + (2/h) x'_i sum_j k_ij],
+//   w_j = s_j - (2/h) x'_j, k_ij = exp(-|x_i-x_j|^2/h), fused in registers
+//   over column chunks with a fixed-order merge (no float atomics).
+#include "fcb_internal.cuh"
+
+#include <algorithm>
+
+namespace fcb {
+
+constexpr double BANDWIDTH_FLOOR = 1e-12;  // stein.py:34
+
+// ---------------------------------------------------------------------------
+// Gaussian mixture score / log density
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) gmm_eval_kernel(const double* __restrict__ X, int n, int k,
+                                                       const double* __restrict__ prm,
+                                                       double* __restrict__ score,
+                                                       double* __restrict__ logdens,
+                                                       const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    const double* logw = prm;
+    const double* lognorm = prm + k;
+    const double* mu = prm + 2 * k;
+    const double* chol = prm + 2 * k + (size_t)k * D;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double x[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) x[q] = X[(size_t)i * D + q];
+        double M = -INFINITY, S = 0.0, acc[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc[q] = 0.0;
+        for (int c = 0; c < k; ++c) {
+            const double* L = chol + (size_t)c * D * D;
+            double diff[D], y[D], pull[D];
+#pragma unroll
+            for (int q = 0; q < D; ++q) diff[q] = x[q] - mu[(size_t)c * D + q];
+            // forward substitution L y = diff
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                double v = diff[r];
+#pragma unroll
+                for (int q = 0; q < r; ++q) v -= L[r * D + q] * y[q];
+                y[r] = v / L[r * D + r];
+            }
+            // back substitution L^T pull = y
+#pragma unroll
+            for (int r = D - 1; r >= 0; --r) {
+                double v = y[r];
+#pragma unroll
+                for (int q = r + 1; q < D; ++q) v -= L[q * D + r] * pull[q];
+                pull[r] = v / L[r * D + r];
+            }
+            double quad = 0.0;
+#pragma unroll
+            for (int q = 0; q < D; ++q) quad += diff[q] * pull[q];
+            const double sc = -0.5 * quad - lognorm[c] + logw[c];
+            if (sc > M) {
+                const double r = (S > 0.0) ? exp(M - sc) : 0.0;
+                S = S * r + 1.0;
+#pragma unroll
+                for (int q = 0; q < D; ++q) acc[q] = acc[q] * r + pull[q];
+                M = sc;
+            } else {
+                const double r = exp(sc - M);
+                S += r;
+#pragma unroll
+                for (int q = 0; q < D; ++q) acc[q] += r * pull[q];
+            }
+        }
+        if (score) {
+#pragma unroll
+            for (int q = 0; q < D; ++q) score[(size_t)i * D + q] = -acc[q] / S;
+        }
+        if (logdens) logdens[i] = M + log(S);
+    }
+}
+
+int gmm_eval(const double* X, int n, int d, int k, const double* prm, double* score,
+             double* logdens, const int* gate, cudaStream_t st) {
+    if (n < 1) return FCB_OK;
+    const int blocks = std::min(4 * sm_count(), (n + 255) / 256);
+    switch (d) {
+        case 1: gmm_eval_kernel<1><<<blocks, 256, 0, st>>>(X, n, k, prm, score, logdens, gate); break;
+        case 2: gmm_eval_kernel<2><<<blocks, 256, 0, st>>>(X, n, k, prm, score, logdens, gate); break;
+        case 3: gmm_eval_kernel<3><<<blocks, 256, 0, st>>>(X, n, k, prm, score, logdens, gate); break;
+        default: return fail(FCB_ENOTSUP, "gmm dimension must be 1, 2 or 3");
+    }
+    FCB_LAUNCHED("gmm_eval_kernel");
+    return FCB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exact median of the n^2 pairwise distances (radix select)
+// ---------------------------------------------------------------------------
+constexpr int MED_TILE = 64;
+constexpr int MED_BLOCK = 256;
+constexpr int MED_BINS = 2048;
+constexpr int MED_PASSES = 6;
+__constant__ int c_med_shift[MED_PASSES] = {52, 41, 30, 19, 8, 0};
+__constant__ int c_med_bits[MED_PASSES] = {11, 11, 11, 11, 11, 8};
+
+struct MedState {
+    unsigned long long prefix[2];  // selected high bits so far (lo, hi target)
+    unsigned long long rank[2];    // remaining rank inside the prefix bucket
+    unsigned long long hist[2][MED_BINS];
+};
+
+template <int D>
+__device__ __forceinline__ unsigned long long sqdist_key(const double* a, const double* b) {
+    // (a0-b0)^2 + (a1-b1)^2 [+ (a2-b2)^2], left to right, no contraction
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+        const double df = __dsub_rn(a[q], b[q]);
+        const double sq = __dmul_rn(df, df);
+        acc = (q == 0) ? sq : __dadd_rn(acc, sq);
+    }
+    return (unsigned long long)__double_as_longlong(acc);
+}
+
+template <int D>
+__global__ void __launch_bounds__(MED_BLOCK) median_hist_kernel(const double* __restrict__ X, int n,
+                                                                MedState* st, int pass,
+                                                                const int* gate) {
+    __shared__ unsigned hist[2][MED_BINS];
+    __shared__ double pj[MED_TILE * D];
+    if (gate && *((volatile const int*)gate) != 0) return;
+    const int shift = c_med_shift[pass];
+    const int bits = c_med_bits[pass];
+    const int hshift = shift + bits;  // bits above the current digit are known
+    const unsigned long long pre0 = st->prefix[0], pre1 = st->prefix[1];
+    const bool same = pre0 == pre1;
+    for (int b = threadIdx.x; b < 2 * MED_BINS; b += MED_BLOCK) (&hist[0][0])[b] = 0u;
+    const int nb = (n + MED_TILE - 1) / MED_TILE;
+    const long long ntiles = (long long)nb * (nb + 1) / 2;
+    __syncthreads();
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        // map t -> (bi, bj) with bi <= bj (row-major upper triangle)
+        int bi = (int)((2.0 * nb + 1.0 - sqrt((2.0 * nb + 1.0) * (2.0 * nb + 1.0) - 8.0 * t)) / 2.0);
+        bi = max(0, min(bi, nb - 1));
+        while (bi > 0 && (long long)bi * nb - (long long)bi * (bi - 1) / 2 > t) --bi;
+        while ((long long)(bi + 1) * nb - (long long)(bi + 1) * bi / 2 <= t) ++bi;
+        const long long row_start = (long long)bi * nb - (long long)bi * (bi - 1) / 2;
+        const int bj = bi + (int)(t - row_start);
+        __syncthreads();
+        for (int k = threadIdx.x; k < MED_TILE * D; k += MED_BLOCK) {
+            const int j = bj * MED_TILE + k / D;
+            pj[k] = (j < n) ? X[(size_t)j * D + (k % D)] : 0.0;
+        }
+        __syncthreads();
+        // each thread: one i row (64 rows / 4 threads per row) x 16 columns
+        const int il = threadIdx.x >> 2;
+        const int jq = threadIdx.x & 3;
+        const int i = bi * MED_TILE + il;
+        if (i < n) {
+            double xi[D];
+#pragma unroll
+            for (int q = 0; q < D; ++q) xi[q] = X[(size_t)i * D + q];
+            for (int jj = jq; jj < MED_TILE; jj += 4) {
+                const int j = bj * MED_TILE + jj;
+                if (j >= n || j <= i) continue;
+                const unsigned long long key = sqdist_key<D>(xi, &pj[jj * D]);
+                const unsigned long long hi = (hshift >= 64) ? 0ull : (key >> hshift);
+                const unsigned dig = (unsigned)((key >> shift) & ((1ull << bits) - 1ull));
+                if (hi == pre0) atomicAdd(&hist[0][dig], 2u);
+                if (!same && hi == pre1) atomicAdd(&hist[1][dig], 2u);
+            }
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < MED_BINS; b += MED_BLOCK) {
+        if (hist[0][b]) atomicAdd(&st->hist[0][b], (unsigned long long)hist[0][b]);
+        if (!same && hist[1][b]) atomicAdd(&st->hist[1][b], (unsigned long long)hist[1][b]);
+    }
+}
+
+__global__ void median_init_kernel(MedState* st, unsigned long long klo, unsigned long long khi,
+                                   const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    for (int b = threadIdx.x; b < 2 * MED_BINS; b += blockDim.x) (&st->hist[0][0])[b] = 0ull;
+    if (threadIdx.x == 0) {
+        st->prefix[0] = st->prefix[1] = 0ull;
+        st->rank[0] = klo;
+        st->rank[1] = khi;
+    }
+}
+
+__global__ void median_select_kernel(MedState* st, int n, int pass, const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    if (threadIdx.x == 0) {
+        const int bits = c_med_bits[pass];
+        const int nbins = 1 << bits;
+        const bool same = st->prefix[0] == st->prefix[1];
+        for (int t = 0; t < 2; ++t) {
+            unsigned long long* h = st->hist[same ? 0 : t];
+            // the n diagonal zeros live in bucket 0 while the prefix is 0
+            const unsigned long long zeros = (st->prefix[t] == 0ull) ? (unsigned long long)n : 0ull;
+            unsigned long long r = st->rank[t];
+            int b = 0;
+            for (; b < nbins; ++b) {
+                const unsigned long long c = h[b] + (b == 0 ? zeros : 0ull);
+                if (r < c) break;
+                r -= c;
+            }
+            if (b >= nbins) b = nbins - 1;  // unreachable for consistent counts
+            st->rank[t] = r;
+            st->prefix[t] = (st->prefix[t] << bits) | (unsigned long long)b;
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 2 * MED_BINS; b += blockDim.x) (&st->hist[0][0])[b] = 0ull;
+}
+
+__global__ void median_finish_kernel(const MedState* st, int n, double log_np1, double* hstat,
+                                     const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    if (threadIdx.x != 0) return;
+    const double vlo = __longlong_as_double((long long)st->prefix[0]);
+    const double vhi = __longlong_as_double((long long)st->prefix[1]);
+    const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
+    double med;
+    if (N % 2ull == 1ull) med = sqrt(vlo);
+    else med = __ddiv_rn(__dadd_rn(sqrt(vlo), sqrt(vhi)), 2.0);
+    double h = __ddiv_rn(__dmul_rn(med, med), log_np1);
+    const bool clamped = h <= BANDWIDTH_FLOOR;
+    if (clamped) h = BANDWIDTH_FLOOR;
+    hstat[0] = h;
+    hstat[1] = med;
+    hstat[2] = clamped ? 1.0 : 0.0;
+    hstat[3] = 0.0;
+}
+
+__global__ void fixed_bandwidth_kernel(double h, double* hstat, const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    if (threadIdx.x == 0) {
+        const bool clamped = h <= BANDWIDTH_FLOOR;
+        hstat[0] = clamped ? BANDWIDTH_FLOOR : h;
+        hstat[1] = NAN;
+        hstat[2] = clamped ? 1.0 : 0.0;
+        hstat[3] = 0.0;
+    }
+}
+
+size_t median_ws_bytes(int n) {
+    (void)n;
+    return align_up(sizeof(MedState), 256);
+}
+
+int median_bandwidth(const double* X, int n, int d, double log_np1, double* hstat, const int* gate,
+                     void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (n < 1) return fail(FCB_EINPUT, "need at least one point");
+    if (ws_bytes < median_ws_bytes(n)) return fail(FCB_EWORKSPACE, "median workspace too small");
+    if (n == 1) {  // stein.py:73-74
+        fixed_bandwidth_kernel<<<1, 32, 0, st>>>(1.0, hstat, gate);
+        FCB_LAUNCHED("fixed_bandwidth_kernel");
+        return FCB_OK;
+    }
+    MedState* ms = static_cast<MedState*>(ws);
+    const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
+    median_init_kernel<<<1, 256, 0, st>>>(ms, (N - 1ull) / 2ull, N / 2ull, gate);
+    FCB_LAUNCHED("median_init_kernel");
+    const int nb = (n + MED_TILE - 1) / MED_TILE;
+    const long long ntiles = (long long)nb * (nb + 1) / 2;
+    const int grid = (int)std::min<long long>(ntiles, 4LL * sm_count());
+    for (int pass = 0; pass < MED_PASSES; ++pass) {
+        switch (d) {
+            case 1: median_hist_kernel<1><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate); break;
+            case 2: median_hist_kernel<2><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate); break;
+            case 3: median_hist_kernel<3><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate); break;
+            default: return fail(FCB_ENOTSUP, "dimension must be 1, 2 or 3");
+        }
+        FCB_LAUNCHED("median_hist_kernel");
+        median_select_kernel<<<1, 256, 0, st>>>(ms, n, pass, gate);
+        FCB_LAUNCHED("median_select_kernel");
+    }
+    median_finish_kernel<<<1, 32, 0, st>>>(ms, n, log_np1, hstat, gate);
+    FCB_LAUNCHED("median_finish_kernel");
+    return FCB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Stein flow
+// ---------------------------------------------------------------------------
+constexpr int SV_BLOCK = 256;
+constexpr int SV_TILE = 256;
+constexpr int SV_SUB = 8;
+constexpr int SV_MAXCH = 64;
+
+template <typename Real>
+struct alignas(sizeof(Real) * 4) SvCol {
+    Real x[4];  // scaled centred coordinates (x[3] unused)
+    Real w[4];  // w_j = s_j - (2/h) x'_j           (w[3] unused)
+};
+
+struct SvPlan {
+    int n, nrb, nchunks, chunk_len, items, n8;
+};
+
+static SvPlan sv_plan(int n, int rpt, int grid) {
+    SvPlan p{};
+    p.n = n;
+    p.n8 = (n + SV_SUB - 1) / SV_SUB * SV_SUB;
+    const int br = SV_BLOCK * rpt;
+    p.nrb = (n + br - 1) / br;
+    const int maxch = std::max(1, std::min(SV_MAXCH, p.n8 / 64));
+    int best = 1;
+    double best_eff = -1.0;
+    for (int k = 1; k <= maxch; ++k) {
+        const long items = (long)p.nrb * k;
+        const long waves = (items + grid - 1) / grid;
+        const double eff = (double)items / (double)(waves * grid);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = k;
+        }
+        if (eff > 0.97) break;
+    }
+    int cl = (p.n8 + best - 1) / best;
+    cl = (cl + SV_SUB - 1) / SV_SUB * SV_SUB;
+    p.chunk_len = cl;
+    p.nchunks = (p.n8 + cl - 1) / cl;
+    p.items = p.nrb * p.nchunks;
+    return p;
+}
+
+template <typename Real, int D>
+__global__ void sv_pack_kernel(const double* __restrict__ X, int n, int n8,
+                               const double* __restrict__ score, const double* __restrict__ hstat,
+                               const double* __restrict__ centre, SvCol<Real>* __restrict__ cols,
+                               Vec4<Real>* __restrict__ rows, const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    const double h = hstat[0];
+    const double unit = (sizeof(Real) == 4) ? kLog2e : 1.0;
+    const double sc = sqrt(unit / h);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n8; j += gridDim.x * blockDim.x) {
+        SvCol<Real> c{};
+        Vec4<Real> r{};
+        if (j < n) {
+            Real xs[3] = {0, 0, 0};
+            for (int q = 0; q < D; ++q) {
+                const double xc = X[(size_t)j * D + q] - centre[q];
+                c.x[q] = (Real)(xc * sc);
+                c.w[q] = (Real)(score[(size_t)j * D + q] - (2.0 / h) * xc);
+                xs[q] = c.x[q];
+            }
+            r = Vec4<Real>{xs[0], xs[1], xs[2], 0};
+            rows[j] = r;
+        } else {
+            for (int q = 0; q < 4; ++q) {
+                c.x[q] = (Real)1e30;  // padding: distance -> inf, kernel weight -> 0
+                c.w[q] = 0;
+            }
+        }
+        cols[j] = c;
+    }
+}
+
+template <typename Real, int D, int RPT>
+__global__ void __launch_bounds__(SV_BLOCK) sv_sweep_kernel(SvPlan pl,
+                                                            const Vec4<Real>* __restrict__ rows,
+                                                            const SvCol<Real>* __restrict__ cols,
+                                                            Real* __restrict__ part,
+                                                            const int* gate) {
+    using U = Units<Real>;
+    __shared__ SvCol<Real> tile[SV_TILE];
+    if (gate && *((volatile const int*)gate) != 0) return;
+    const int n = pl.n;
+    for (int item = blockIdx.x; item < pl.items; item += gridDim.x) {
+        const int rb = item % pl.nrb, ch = item / pl.nrb;
+        const int c0 = ch * pl.chunk_len, c1 = min(c0 + pl.chunk_len, pl.n8);
+        const int row0 = rb * SV_BLOCK * RPT;
+        Real x[RPT][D], ks[RPT], acc[RPT][D];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int i = min(row0 + r * SV_BLOCK + threadIdx.x, n - 1);
+            const Vec4<Real> v = rows[i];
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                x[r][q] = vget(v, q);
+                acc[r][q] = 0;
+            }
+            ks[r] = 0;
+        }
+        for (int t0 = c0; t0 < c1; t0 += SV_TILE) {
+            const int len = min(SV_TILE, c1 - t0);
+            __syncthreads();
+            for (int k = threadIdx.x; k < len; k += SV_BLOCK) tile[k] = cols[t0 + k];
+            __syncthreads();
+            for (int c = 0; c < len; c += SV_SUB) {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    Real ts = 0, ta[D];
+#pragma unroll
+                    for (int q = 0; q < D; ++q) ta[q] = 0;
+#pragma unroll
+                    for (int k = 0; k < SV_SUB; ++k) {
+                        const SvCol<Real>& cc = tile[c + k];
+                        Real d2 = 0;
+#pragma unroll
+                        for (int q = 0; q < D; ++q) {
+                            const Real df = x[r][q] - cc.x[q];
+                            d2 = fma(df, df, d2);
+                        }
+                        const Real e = U::expu(-d2);
+                        ts += e;
+#pragma unroll
+                        for (int q = 0; q < D; ++q) ta[q] = fma(e, cc.w[q], ta[q]);
+                    }
+                    ks[r] += ts;
+#pragma unroll
+                    for (int q = 0; q < D; ++q) acc[r][q] += ta[q];
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int i = row0 + r * SV_BLOCK + threadIdx.x;
+            if (i < n) {
+                part[((size_t)ch * (D + 1)) * n + i] = ks[r];
+#pragma unroll
+                for (int q = 0; q < D; ++q) part[((size_t)ch * (D + 1) + 1 + q) * n + i] = acc[r][q];
+            }
+        }
+    }
+}
+
+template <typename Real, int D>
+__global__ void sv_merge_kernel(SvPlan pl, const Real* __restrict__ part,
+                                const double* __restrict__ X, const double* __restrict__ hstat,
+                                const double* __restrict__ centre, double* __restrict__ out,
+                                const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    const int n = pl.n;
+    const double h = hstat[0];
+    const double two_over_h = 2.0 / h, inv_n = 1.0 / n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double K = 0.0, A[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) A[q] = 0.0;
+        for (int ch = 0; ch < pl.nchunks; ++ch) {
+            K += (double)part[((size_t)ch * (D + 1)) * n + i];
+#pragma unroll
+            for (int q = 0; q < D; ++q) A[q] += (double)part[((size_t)ch * (D + 1) + 1 + q) * n + i];
+        }
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            const double xc = X[(size_t)i * D + q] - centre[q];
+            out[(size_t)i * D + q] = inv_n * (A[q] + two_over_h * xc * K);
+        }
+    }
+}
+
+constexpr int SV_RPT_F32 = 2;
+constexpr int SV_RPT_F64 = 1;
+
+struct SvWs {
+    double* centre;
+    void* cols;
+    void* rows;
+    void* part;
+    size_t total;
+};
+
+static SvWs sv_layout(int precision, int n, int d, SvPlan pl, void* ws, size_t bytes) {
+    Arena ar(ws, bytes);
+    SvWs L{};
+    L.centre = ar.take<double>(4);
+    if (precision == FCB_FP64) {
+        L.cols = ar.take<SvCol<double>>(pl.n8);
+        L.rows = ar.take<Vec4<double>>(n);
+        L.part = ar.take<double>((size_t)pl.nchunks * (d + 1) * n);
+    } else {
+        L.cols = ar.take<SvCol<float>>(pl.n8);
+        L.rows = ar.take<Vec4<float>>(n);
+        L.part = ar.take<float>((size_t)pl.nchunks * (d + 1) * n);
+    }
+    L.total = ar.off + 256;
+    return L;
+}
+
+static int sv_grid() { return 2 * sm_count(); }
+
+size_t stein_ws_bytes(int precision, int n, int d) {
+    const int rpt = precision == FCB_FP64 ? SV_RPT_F64 : SV_RPT_F32;
+    SvPlan pl = sv_plan(n, rpt, sv_grid());
+    return sv_layout(precision, n, d, pl, nullptr, 0).total;
+}
+
+template <typename Real, int D, int RPT>
+static int stein_run(const double* X, int n, const double* scores, const double* hstat,
+                     double* out, const int* gate, void* ws, size_t ws_bytes, cudaStream_t st) {
+    const int precision = sizeof(Real) == 8 ? FCB_FP64 : FCB_FP32;
+    SvPlan pl = sv_plan(n, RPT, sv_grid());
+    SvWs L = sv_layout(precision, n, D, pl, ws, ws_bytes);
+    if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "stein workspace too small");
+    // centre on the first point: exactly coincident clouds (the degenerate
+    // median case of stein.py:101-103) then have x' == 0 bit-exactly
+    const double* centre = X;
+    const int pb = std::max(1, std::min(4 * sm_count(), (pl.n8 + 255) / 256));
+    sv_pack_kernel<Real, D><<<pb, 256, 0, st>>>(X, n, pl.n8, scores, hstat, centre,
+                                               static_cast<SvCol<Real>*>(L.cols),
+                                               static_cast<Vec4<Real>*>(L.rows), gate);
+    FCB_LAUNCHED("sv_pack_kernel");
+    const int grid = std::min(pl.items, sv_grid());
+    sv_sweep_kernel<Real, D, RPT><<<grid, SV_BLOCK, 0, st>>>(
+        pl, static_cast<const Vec4<Real>*>(L.rows), static_cast<const SvCol<Real>*>(L.cols),
+        static_cast<Real*>(L.part), gate);
+    FCB_LAUNCHED("sv_sweep_kernel");
+    const int mb = std::max(1, std::min(4 * sm_count(), (n + 255) / 256));
+    sv_merge_kernel<Real, D><<<mb, 256, 0, st>>>(pl, static_cast<const Real*>(L.part), X, hstat,
+                                                centre, out, gate);
+    FCB_LAUNCHED("sv_merge_kernel");
+    return FCB_OK;
+}
+
+int stein_flow(int precision, const double* X, int n, int d, const double* scores,
+               const double* hstat, double* out, const int* gate, void* ws, size_t ws_bytes,
+               cudaStream_t st) {
+    if (n < 1) return fail(FCB_EINPUT, "need at least one point");
+#define FCB_SV_CASE(DD)                                                                          \
+    if (d == DD) {                                                                               \
+        if (precision == FCB_FP64)                                                               \
+            return stein_run<double, DD, SV_RPT_F64>(X, n, scores, hstat, out, gate, ws,         \
+                                                     ws_bytes, st);                              \
+        return stein_run<float, DD, SV_RPT_F32>(X, n, scores, hstat, out, gate, ws, ws_bytes,   \
+                                                st);                                             \
+    }
+    FCB_SV_CASE(1)
+    FCB_SV_CASE(2)
+    FCB_SV_CASE(3)
+#undef FCB_SV_CASE
+    return fail(FCB_ENOTSUP, "dimension must be 1, 2 or 3");
+}
+
+// ---------------------------------------------------------------------------
+// planner composite: bandwidth, score, flow, convergence hook
+// ---------------------------------------------------------------------------
+constexpr int SFIN_BLOCK = 1024;
+__global__ void __launch_bounds__(SFIN_BLOCK)
+    stein_finalize_kernel(const double* __restrict__ flow, int n, int d,
+                          const double* __restrict__ hstat, double* fstat, int* plan_state,
+                          int iteration, double* flow_log, double conv_tol) {
+    __shared__ double scratch[32];
+    if (plan_state && *((volatile int*)plan_state) != 0) return;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += SFIN_BLOCK) {
+        double sq = 0.0;
+        for (int q = 0; q < d; ++q) {
+            const double v = flow[(size_t)i * d + q];
+            sq += v * v;
+        }
+        acc += sqrt(sq);
+    }
+    const double total = block_sum<SFIN_BLOCK>(acc, scratch);
+    if (threadIdx.x == 0) {
+        const double mean_mag = total / n;
+        fstat[0] = 0.0;
+        fstat[1] = 1.0;
+        fstat[2] = 0.0;
+        fstat[3] = mean_mag;
+        fstat[4] = hstat[0];
+        fstat[5] = hstat[2];
+        fstat[6] = hstat[1];
+        fstat[7] = 0.0;
+        if (plan_state) {
+            double* lg = flow_log + 4 * (size_t)iteration;
+            lg[0] = mean_mag;
+            lg[1] = hstat[0];
+            lg[2] = hstat[2];
+            lg[3] = hstat[1];
+            plan_state[FCB_STATE_FLOWS] = iteration + 1;
+            if (mean_mag < conv_tol) plan_state[FCB_STATE_STOP] = 1;
+        }
+    }
+}
+
+struct SfWs {
+    double* hstat;
+    double* scores;
+    void* med;
+    void* sv;
+    size_t sv_bytes, total;
+};
+
+static SfWs sf_layout(int precision, int n, int d, void* ws, size_t bytes) {
+    Arena ar(ws, bytes);
+    SfWs L{};
+    L.hstat = ar.take<double>(4);
+    L.scores = ar.take<double>((size_t)n * d);
+    L.med = ar.take<char>(median_ws_bytes(n));
+    L.sv_bytes = stein_ws_bytes(precision, n, d);
+    L.sv = ar.take<char>(L.sv_bytes);
+    L.total = ar.off + 256;
+    return L;
+}
+
+size_t stein_flow_full_ws_bytes(int precision, int n, int d) {
+    return sf_layout(precision, n, d, nullptr, 0).total;
+}
+
+int stein_flow_full(int precision, const double* X, int n, int d, int k, const double* prm,
+                    double bandwidth_fixed, double log_np1, double* flow, double* fstat,
+                    int* plan_state, int iteration, double* flow_log, double conv_tol, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+    SfWs L = sf_layout(precision, n, d, ws, ws_bytes);
+    if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "stein_flow_full workspace too small");
+    int rc;
+    if (bandwidth_fixed > 0.0) {
+        fixed_bandwidth_kernel<<<1, 32, 0, st>>>(bandwidth_fixed, L.hstat, plan_state);
+        FCB_LAUNCHED("fixed_bandwidth_kernel");
+    } else {
+        rc = median_bandwidth(X, n, d, log_np1, L.hstat, plan_state, L.med, median_ws_bytes(n), st);
+        if (rc) return rc;
+    }
+    rc = gmm_eval(X, n, d, k, prm, L.scores, nullptr, plan_state, st);
+    if (rc) return rc;
+    rc = stein_flow(precision, X, n, d, L.scores, L.hstat, flow, plan_state, L.sv, L.sv_bytes, st);
+    if (rc) return rc;
+    stein_finalize_kernel<<<1, SFIN_BLOCK, 0, st>>>(flow, n, d, L.hstat, fstat, plan_state,
+                                                    iteration, flow_log, conv_tol);
+    FCB_LAUNCHED("stein_finalize_kernel");
+    return FCB_OK;
+}
+
+}  // namespace fcb
