@@ -10,6 +10,7 @@
 // The Riccati sweep and the rollout are sequential in time; each problem is
 // one thread with its matrices in registers (n <= 6, m <= 3).
 #include "fcb_internal.cuh"
+#include "lqr_scan.cuh"
 
 #include <algorithm>
 
@@ -137,54 +138,82 @@ __device__ __forceinline__ bool all_finite(const double* v, int n) {
     return ok;
 }
 
+constexpr int RO_CHUNK = 256;
+
+// One warp per rollout: all lanes stage a chunk of controls into shared
+// memory (coalesced), lane 0 integrates the chunk, then all lanes write the
+// states and workspace points back.  The sequential RK4 chain never waits on
+// a global load.
 template <class Mdl>
-__global__ void rollout_kernel(const double* __restrict__ prm, const double* __restrict__ s0,
-                               const double* __restrict__ U, int T, double dt,
-                               double* __restrict__ S, int d, const double* __restrict__ P,
-                               double* __restrict__ X, int* status, int* plan_state, int iteration) {
+__global__ void __launch_bounds__(32) rollout_kernel(const double* __restrict__ prm,
+                                                    const double* __restrict__ s0,
+                                                    const double* __restrict__ U, int T, double dt,
+                                                    double* __restrict__ S, int d,
+                                                    const double* __restrict__ P,
+                                                    double* __restrict__ X, int* status,
+                                                    int* plan_state, int iteration) {
     constexpr int N = Mdl::N, M = Mdl::M;
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    __shared__ double sU[RO_CHUNK * M];
+    __shared__ double sS[RO_CHUNK * N];
+    __shared__ double sP[3 * N];
+    __shared__ int s_fail;
+    const int lane = threadIdx.x;
     if (plan_state && *((volatile int*)plan_state) != 0) return;
-    double s[N], u[M], k1[N], k2[N], k3[N], k4[N], tmp[N];
+    for (int i = lane; i < d * N; i += 32) sP[i] = P ? P[i] : 0.0;
+    if (lane == 0) s_fail = -1;
+    double s[N];
+    for (int j = 0; j < N; ++j) s[j] = s0[j];
+    if (lane < N) S[lane] = s0[lane];
     const double half = DMUL(0.5, dt);
     const double sixth = dt / 6.0;
-    for (int j = 0; j < N; ++j) {
-        s[j] = s0[j];
-        S[j] = s[j];
-    }
-    int fail_step = -1;
-    for (int k = 0; k < T; ++k) {
-        for (int j = 0; j < M; ++j) u[j] = U[(size_t)k * M + j];
-        Mdl::f(s, u, prm, k1);
-        for (int j = 0; j < N; ++j) tmp[j] = DADD(s[j], DMUL(half, k1[j]));
-        Mdl::f(tmp, u, prm, k2);
-        for (int j = 0; j < N; ++j) tmp[j] = DADD(s[j], DMUL(half, k2[j]));
-        Mdl::f(tmp, u, prm, k3);
-        for (int j = 0; j < N; ++j) tmp[j] = DADD(s[j], DMUL(dt, k3[j]));
-        Mdl::f(tmp, u, prm, k4);
-        for (int j = 0; j < N; ++j) {
-            const double inner = DADD(DADD(k1[j], DMUL(2.0, DADD(k2[j], k3[j]))), k4[j]);
-            s[j] = DADD(s[j], DMUL(sixth, inner));
-        }
-        if (!all_finite(s, N)) {
-            fail_step = k + 1;
-            break;
-        }
-        for (int j = 0; j < N; ++j) S[(size_t)(k + 1) * N + j] = s[j];
-        if (X) {
-            for (int r = 0; r < d; ++r) {
-                double a = 0.0;
-                for (int j = 0; j < N; ++j) a = DADD(a, DMUL(s[j], P[r * N + j]));
-                X[(size_t)k * d + r] = a;
+    for (int c0 = 0; c0 < T; c0 += RO_CHUNK) {
+        const int len = min(RO_CHUNK, T - c0);
+        for (int i = lane; i < len * M; i += 32) sU[i] = U[(size_t)c0 * M + i];
+        __syncwarp();
+        if (lane == 0 && s_fail < 0) {
+            double u[M], k1[N], k2[N], k3[N], k4[N], tmp[N];
+            for (int k = 0; k < len; ++k) {
+                for (int j = 0; j < M; ++j) u[j] = sU[k * M + j];
+                Mdl::f(s, u, prm, k1);
+                for (int j = 0; j < N; ++j) tmp[j] = DADD(s[j], DMUL(half, k1[j]));
+                Mdl::f(tmp, u, prm, k2);
+                for (int j = 0; j < N; ++j) tmp[j] = DADD(s[j], DMUL(half, k2[j]));
+                Mdl::f(tmp, u, prm, k3);
+                for (int j = 0; j < N; ++j) tmp[j] = DADD(s[j], DMUL(dt, k3[j]));
+                Mdl::f(tmp, u, prm, k4);
+                for (int j = 0; j < N; ++j) {
+                    const double inner = DADD(DADD(k1[j], DMUL(2.0, DADD(k2[j], k3[j]))), k4[j]);
+                    s[j] = DADD(s[j], DMUL(sixth, inner));
+                }
+                if (!all_finite(s, N)) {
+                    s_fail = c0 + k + 1;
+                    break;
+                }
+                for (int j = 0; j < N; ++j) sS[k * N + j] = s[j];
             }
         }
+        __syncwarp();
+        const int fail = s_fail;
+        const int valid = (fail < 0) ? len : (fail - 1 - c0);
+        for (int i = lane; i < valid * N; i += 32) S[(size_t)(c0 + 1) * N + i] = sS[i];
+        if (X)
+            for (int i = lane; i < valid * d; i += 32) {
+                const int k = i / d, r = i % d;
+                double a = 0.0;
+                for (int j = 0; j < N; ++j) a = DADD(a, DMUL(sS[k * N + j], sP[r * N + j]));
+                X[(size_t)(c0 + k) * d + r] = a;
+            }
+        __syncwarp();
+        if (fail >= 0) break;
     }
-    if (status) *status = fail_step;
-    if (plan_state && fail_step >= 0) {
-        plan_state[FCB_STATE_STOP] = 2;
-        plan_state[FCB_STATE_STAGE] = 1;
-        plan_state[FCB_STATE_ITER] = iteration;
-        plan_state[FCB_STATE_INDEX] = fail_step;
+    if (lane == 0) {
+        if (status) *status = s_fail;
+        if (plan_state && s_fail >= 0) {
+            plan_state[FCB_STATE_STOP] = 2;
+            plan_state[FCB_STATE_STAGE] = 1;
+            plan_state[FCB_STATE_ITER] = iteration;
+            plan_state[FCB_STATE_INDEX] = s_fail;
+        }
     }
 }
 
@@ -206,55 +235,6 @@ __global__ void linearize_kernel(const double* __restrict__ prm, const double* _
 // ---------------------------------------------------------------------------
 // flow-matching LQR (lqr.py:154-200)
 // ---------------------------------------------------------------------------
-// Solve H X = R (H: m x m, R: m x c) by Gaussian elimination with partial
-// pivoting (the LAPACK gesv algorithm np.linalg.solve uses).
-template <int M, int C>
-__device__ __forceinline__ void solve_small(double (&H)[M][M], double (&R)[M][C]) {
-#pragma unroll
-    for (int col = 0; col < M; ++col) {
-        int piv = col;
-        double best = fabs(H[col][col]);
-#pragma unroll
-        for (int r = col + 1; r < M; ++r)
-            if (fabs(H[r][col]) > best) {
-                best = fabs(H[r][col]);
-                piv = r;
-            }
-        if (piv != col) {
-#pragma unroll
-            for (int k = 0; k < M; ++k) {
-                double t = H[col][k];
-                H[col][k] = H[piv][k];
-                H[piv][k] = t;
-            }
-#pragma unroll
-            for (int k = 0; k < C; ++k) {
-                double t = R[col][k];
-                R[col][k] = R[piv][k];
-                R[piv][k] = t;
-            }
-        }
-#pragma unroll
-        for (int r = col + 1; r < M; ++r) {
-            const double l = H[r][col] / H[col][col];
-#pragma unroll
-            for (int k = col; k < M; ++k) H[r][k] -= l * H[col][k];
-#pragma unroll
-            for (int k = 0; k < C; ++k) R[r][k] -= l * R[col][k];
-        }
-    }
-#pragma unroll
-    for (int r = M - 1; r >= 0; --r) {
-#pragma unroll
-        for (int k = 0; k < C; ++k) {
-            double v = R[r][k];
-#pragma unroll
-            for (int q = r + 1; q < M; ++q) v -= H[r][q] * R[q][k];
-            R[r][k] = v / H[r][r];
-        }
-    }
-}
-
 // Source of per-step Jacobians: explicit arrays or a model evaluated along
 // (S, U) on the fly.
 template <int N, int M>
@@ -303,206 +283,24 @@ struct LiftedFlow {
     }
 };
 
-template <int N, int M, class Jac, class Flow>
-__device__ void lqr_core(const Jac& jac, const Flow& flow, int T, double dt,
-                         const double* __restrict__ Qm, const double* __restrict__ Rm,
-                         double* __restrict__ Kout, double* __restrict__ dout,
-                         double* __restrict__ v, double* __restrict__ z, double* cost_out,
-                         int* fail_out) {
-    double Qb[N][N], Rb[M][M];
-    for (int i = 0; i < N; ++i)
-        for (int j = 0; j < N; ++j) Qb[i][j] = dt * Qm[i * N + j];
-    for (int i = 0; i < M; ++i)
-        for (int j = 0; j < M; ++j) Rb[i][j] = dt * Rm[i * M + j];
-    double P[N][N], p[N];
-    for (int i = 0; i < N; ++i) {
-        p[i] = 0.0;
-        for (int j = 0; j < N; ++j) P[i][j] = 0.0;
-    }
-    int fail = -1;
-    for (int k = T - 1; k >= 0; --k) {
-        double a[N * N], b[N * M], ak[N];
-        jac.get(k, a, b);
-        flow.get(k, ak);
-        double F[N][N], G[N][M];
-        for (int i = 0; i < N; ++i) {
-            for (int j = 0; j < N; ++j) F[i][j] = (i == j ? 1.0 : 0.0) + dt * a[i * N + j];
-            for (int j = 0; j < M; ++j) G[i][j] = dt * b[i * M + j];
-        }
-        double PG[N][M], PF[N][N];
-        for (int i = 0; i < N; ++i) {
-            for (int j = 0; j < M; ++j) {
-                double s = 0.0;
-                for (int q = 0; q < N; ++q) s += P[i][q] * G[q][j];
-                PG[i][j] = s;
-            }
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-                for (int q = 0; q < N; ++q) s += P[i][q] * F[q][j];
-                PF[i][j] = s;
-            }
-        }
-        double H[M][M], rhs[M][N + 1];
-        for (int i = 0; i < M; ++i) {
-            for (int j = 0; j < M; ++j) {
-                double s = 0.0;
-                for (int q = 0; q < N; ++q) s += G[q][i] * PG[q][j];
-                H[i][j] = Rb[i][j] + s;
-            }
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-                for (int q = 0; q < N; ++q) s += G[q][i] * PF[q][j];
-                rhs[i][j] = s;
-            }
-            double s = 0.0;
-            for (int q = 0; q < N; ++q) s += G[q][i] * p[q];
-            rhs[i][N] = -s;
-        }
-        solve_small<M, N + 1>(H, rhs);
-        for (int i = 0; i < M; ++i) {
-            for (int j = 0; j < N; ++j) Kout[((size_t)k * M + i) * N + j] = rhs[i][j];
-            dout[(size_t)k * M + i] = rhs[i][N];
-        }
-        double FGK[N][N];
-        for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-                for (int q = 0; q < M; ++q) s += G[i][q] * rhs[q][j];
-                FGK[i][j] = F[i][j] - s;
-            }
-        double PFGK[N][N];
-        for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-                for (int q = 0; q < N; ++q) s += P[i][q] * FGK[q][j];
-                PFGK[i][j] = s;
-            }
-        double Pn[N][N];
-        for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-                for (int q = 0; q < N; ++q) s += F[q][i] * PFGK[q][j];
-                Pn[i][j] = Qb[i][j] + s;
-            }
-        bool finite = true;
-        for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) {
-                P[i][j] = 0.5 * (Pn[i][j] + Pn[j][i]);
-                finite = finite && isfinite(P[i][j]);
-            }
-        double pn[N];
-        for (int i = 0; i < N; ++i) {
-            double qa = 0.0;
-            for (int q = 0; q < N; ++q) qa += Qb[i][q] * ak[q];
-            double s = 0.0;
-            for (int q = 0; q < N; ++q) s += FGK[q][i] * p[q];
-            pn[i] = -qa + s;
-        }
-        for (int i = 0; i < N; ++i) {
-            p[i] = pn[i];
-            finite = finite && isfinite(p[i]);
-        }
-        if (!finite) {
-            fail = k;
-            break;
-        }
-    }
-    if (fail_out) *fail_out = fail;
-    if (fail >= 0) return;
-    double zz[N];
-    for (int i = 0; i < N; ++i) {
-        zz[i] = 0.0;
-        if (z) z[i] = 0.0;
-    }
-    double cost = 0.0;
-    for (int k = 0; k < T; ++k) {
-        double a[N * N], b[N * M], ak[N];
-        jac.get(k, a, b);
-        flow.get(k, ak);
-        double vk[M];
-        for (int i = 0; i < M; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < N; ++j) s += Kout[((size_t)k * M + i) * N + j] * zz[j];
-            vk[i] = dout[(size_t)k * M + i] - s;
-            v[(size_t)k * M + i] = vk[i];
-        }
-        double e[N];
-        for (int i = 0; i < N; ++i) e[i] = ak[i] - zz[i];
-        double c1 = 0.0;
-        for (int i = 0; i < N; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < N; ++j) s += Qb[i][j] * e[j];
-            c1 += e[i] * s;
-        }
-        double c2 = 0.0;
-        for (int i = 0; i < M; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < M; ++j) s += Rb[i][j] * vk[j];
-            c2 += vk[i] * s;
-        }
-        cost += c1 + c2;
-        double zn[N];
-        for (int i = 0; i < N; ++i) {
-            double s1 = 0.0;
-            for (int j = 0; j < N; ++j) s1 += ((i == j ? 1.0 : 0.0) + dt * a[i * N + j]) * zz[j];
-            double s2 = 0.0;
-            for (int j = 0; j < M; ++j) s2 += (dt * b[i * M + j]) * vk[j];
-            zn[i] = s1 + s2;
-        }
-        for (int i = 0; i < N; ++i) {
-            zz[i] = zn[i];
-            if (z) z[(size_t)(k + 1) * N + i] = zz[i];
-        }
-    }
-    *cost_out = cost;
-}
-
 template <int N, int M>
-__global__ void lqr_solve_kernel(int T, double dt, const double* A, const double* B,
-                                 const double* Q, const double* R, const double* a, double* v,
-                                 double* z, double* K, double* dff, double* scal, int* status) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(LQR_THREADS) lqr_solve_kernel(LqrScanArgs p, const double* A,
+                                                                 const double* B, const double* a) {
     ArrayJac<N, M> jac{A, B};
     ArrayFlow<N> fl{a};
-    double cost = 0.0;
-    lqr_core<N, M>(jac, fl, T, dt, Q, R, K, dff, v, z, &cost, status);
-    scal[0] = cost;
-    scal[1] = 0.0;
+    lqr_scan_body<N, M>(jac, fl, p);
 }
 
 template <class Mdl>
-__global__ void plan_update_kernel(const double* prm, const double* S, const double* U, int T,
-                                   double dt, int d, const double* P, const double* flow,
-                                   const double* Q, const double* R, double eta,
-                                   const double* clamp, double* Unext, double* lqr_costs,
-                                   int* plan_state, int iteration, double* K, double* dff,
-                                   double* v) {
-    constexpr int N = Mdl::N, M = Mdl::M;
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (plan_state && *((volatile int*)plan_state) != 0) return;
+__global__ void __launch_bounds__(LQR_THREADS) plan_update_kernel(LqrScanArgs p, const double* prm,
+                                                                   const double* S, const double* U,
+                                                                   const double* flow,
+                                                                   const double* P, int d) {
+    constexpr int N = Mdl::N;
+    if (p.plan_state && *((volatile int*)p.plan_state) != 0) return;
     ModelJac<Mdl> jac{prm, S, U};
     LiftedFlow<N> fl{flow, P, d};
-    double cost = 0.0;
-    int fail = -1;
-    lqr_core<N, M>(jac, fl, T, dt, Q, R, K, dff, v, nullptr, &cost, &fail);
-    if (fail >= 0) {
-        plan_state[FCB_STATE_STOP] = 2;
-        plan_state[FCB_STATE_STAGE] = 3;
-        plan_state[FCB_STATE_ITER] = iteration;
-        plan_state[FCB_STATE_INDEX] = fail;
-        return;
-    }
-    lqr_costs[iteration] = cost;
-    for (int k = 0; k < T; ++k)
-        for (int j = 0; j < M; ++j) {
-            double u = U[(size_t)k * M + j] + eta * v[(size_t)k * M + j];
-            if (clamp) {
-                const double b = clamp[j];
-                u = fmin(fmax(u, -b), b);
-            }
-            Unext[(size_t)k * M + j] = u;
-        }
-    plan_state[FCB_STATE_UPDATES] = iteration + 1;
+    lqr_scan_body<N, Mdl::M>(jac, fl, p);
 }
 
 // ---------------------------------------------------------------------------
@@ -584,21 +382,48 @@ int linearize(int model, int ns, int m, const double* prm, const double* S, cons
     return FCB_OK;
 }
 
+// scan scratch: ping-pong aggregates + affine maps, then K and d
+static size_t scan_scratch_doubles(int ns) {
+    const size_t esz = 3 * (size_t)ns * ns + 2 * ns;
+    const size_t asz = (size_t)ns * ns + ns;
+    return 2 * LQR_THREADS * esz + 2 * LQR_THREADS * asz;
+}
+
 size_t lqr_ws_bytes(int ns, int m, int T) {
-    return sizeof(double) * ((size_t)T * m * ns + (size_t)T * m + (size_t)T * m) + 256;
+    return sizeof(double) * (scan_scratch_doubles(ns) + (size_t)T * m * ns + (size_t)T * m) + 512;
+}
+
+static LqrScanArgs scan_args(int ns, int m, int T, double dt, const double* Q, const double* R,
+                             double* ws) {
+    LqrScanArgs p{};
+    const size_t esz = 3 * (size_t)ns * ns + 2 * ns;
+    p.T = T;
+    p.dt = dt;
+    p.Q = Q;
+    p.R = R;
+    p.agg = ws;
+    p.aff = ws + 2 * LQR_THREADS * esz;
+    double* tail = ws + scan_scratch_doubles(ns);
+    p.K = tail;
+    p.dff = tail + (size_t)T * m * ns;
+    return p;
 }
 
 int lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B, const double* Q,
               const double* R, const double* a, double* v, double* z, double* K, double* dff,
               double* scal, int* status, double* ws, cudaStream_t st) {
     if (T < 1) return fail(FCB_EINPUT, "horizon must be >= 1");
-    double* Kb = K ? K : ws;
-    double* db = dff ? dff : ws + (size_t)T * m * ns;
-    if ((!K || !dff) && !ws) return fail(FCB_EWORKSPACE, "lqr needs a workspace for K/d");
-#define FCB_LQR_CASE(NN, MM)                                                                     \
-    case NN * 4 + MM:                                                                            \
-        lqr_solve_kernel<NN, MM><<<1, 32, 0, st>>>(T, dt, A, B, Q, R, a, v, z, Kb, db, scal,      \
-                                                   status);                                      \
+    if (!ws) return fail(FCB_EWORKSPACE, "lqr needs a workspace (fcb_lqr_workspace_bytes)");
+    LqrScanArgs p = scan_args(ns, m, T, dt, Q, R, ws);
+    if (K) p.K = K;
+    if (dff) p.dff = dff;
+    p.v = v;
+    p.z = z;
+    p.cost = scal;
+    p.fail = status;
+#define FCB_LQR_CASE(NN, MM)                                                          \
+    case NN * 4 + MM:                                                                 \
+        lqr_solve_kernel<NN, MM><<<1, LQR_THREADS, 0, st>>>(p, A, B, a);              \
         break;
     switch (ns * 4 + m) {
         FCB_LQR_CASE(1, 1) FCB_LQR_CASE(1, 2) FCB_LQR_CASE(1, 3)
@@ -614,9 +439,7 @@ int lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B,
     return FCB_OK;
 }
 
-size_t plan_update_ws_bytes(int ns, int m, int T) {
-    return sizeof(double) * ((size_t)T * m * ns + 2 * (size_t)T * m) + 512;
-}
+size_t plan_update_ws_bytes(int ns, int m, int T) { return lqr_ws_bytes(ns, m, T) + 256; }
 
 int plan_update(int model, int ns, int m, const double* prm, const double* S, const double* U,
                 int T, double dt, int d, const double* P, const double* flow, const double* Q,
@@ -626,12 +449,19 @@ int plan_update(int model, int ns, int m, const double* prm, const double* S, co
     if (rc) return rc;
     if (ws_bytes < plan_update_ws_bytes(ns, m, T))
         return fail(FCB_EWORKSPACE, "plan_update workspace too small");
-    double* K = ws;
-    double* dff = K + (size_t)T * m * ns;
-    double* v = dff + (size_t)T * m;
-    FCB_MODEL_DISPATCH((plan_update_kernel<Mdl><<<1, 32, 0, st>>>(
-        prm, S, U, T, dt, d, P, flow, Q, R, eta, clamp, Unext, lqr_costs, plan_state, iteration, K,
-        dff, v)));
+    LqrScanArgs p = scan_args(ns, m, T, dt, Q, R, ws);
+    // the status word lives after the scan scratch
+    int* fail_word = reinterpret_cast<int*>(ws + (lqr_ws_bytes(ns, m, T) - 512) / sizeof(double));
+    p.fail = fail_word;
+    p.U = U;
+    p.U_next = Unext;
+    p.eta = eta;
+    p.clamp = clamp;
+    p.lqr_costs = lqr_costs;
+    p.plan_state = plan_state;
+    p.iteration = iteration;
+    FCB_MODEL_DISPATCH((plan_update_kernel<Mdl><<<1, LQR_THREADS, 0, st>>>(p, prm, S, U, flow, P,
+                                                                           d)));
     FCB_LAUNCHED("plan_update_kernel");
     return FCB_OK;
 }

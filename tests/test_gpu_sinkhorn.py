@@ -52,7 +52,9 @@ def test_entropic_ot_golden(precision):
         assert sol.converged == bool(scal[2]) or abs(sol.marginal_error - cfg.tol) < 0.05 * cfg.tol
         assert sol.cost == pytest.approx(scal[0], rel=max(tol, 1e-10), abs=1e-12)
         if f"c{k}_plan" in g:
-            np.testing.assert_allclose(sol.plan(), g[f"c{k}_plan"], rtol=1e-8, atol=1e-12)
+            # exp((f+g-C)/w) amplifies potential errors by 1/w
+            rtol = 1e-8 if tol < 1e-6 else 1e-3
+            np.testing.assert_allclose(sol.plan(), g[f"c{k}_plan"], rtol=rtol, atol=1e-12)
 
 
 @pytest.mark.parametrize("precision", ["float32", "float64"])
@@ -70,9 +72,11 @@ def test_flow_golden_and_warm_state():
         warm = fc.SinkhornWarmState()
         first = fc.sinkhorn_flow(X, fc.SamplePoints(Y), cfg, warm=warm)
         assert rel_inf(first.a, g[f"c{k}_a"]) <= FLOW_TOL, (k, rel_inf(first.a, g[f"c{k}_a"]))
-        assert rel_inf(warm.f, g[f"c{k}_warm_f"]) <= FLOW_TOL
         second = fc.sinkhorn_flow(g[f"c{k}_X2"], fc.SamplePoints(Y), cfg, warm=warm)
         assert rel_inf(second.a, g[f"c{k}_a2"]) <= FLOW_TOL, k
+        # the golden warm state is the one left by the second call
+        assert rel_inf(warm.f, g[f"c{k}_warm_f"]) <= FLOW_TOL, (k, rel_inf(warm.f, g[f"c{k}_warm_f"]))
+        assert rel_inf(warm.p, g[f"c{k}_warm_p"]) <= FLOW_TOL, k
         assert first.converged == bool(g[f"c{k}_scal"][0])
         if f"c{k}_div" in g:
             d = fc.sinkhorn_divergence(X, Y, cfg)
@@ -249,4 +253,6 @@ def test_ragged_and_tiny_shapes():
         f32 = fc.entropic_ot(X, Y, fc.SinkhornConfig(omega=0.05, max_iters=30, tol=1e-300,
                                                      precision="float32"))
         r = O.entropic_ot(X, Y, 0.05, 30, 1e-300)
-        assert rel_inf(f32.f, r["f"]) <= FLOW_TOL, (n, m)
+        scale = max(np.abs(r["f"]).max(), np.abs(r["g"]).max())  # f may vanish (n = 1)
+        assert np.abs(f32.f - r["f"]).max() <= FLOW_TOL * scale, (n, m)
+        assert np.abs(f32.g - r["g"]).max() <= FLOW_TOL * scale, (n, m)
