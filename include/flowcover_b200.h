@@ -194,10 +194,17 @@ FCB_API int fcb_stein_flow_full(int precision, const double* X, int n, int d, in
  * (project_states, dynamics.py:67-69; P is d*ns, device).
  * status: device int; -1 on success, else the step index k+1 of the first
  * non-finite state (RolloutDivergenceError.step).  plan_state/iteration:
- * nullable planner hooks (stage 1). model_params: LTI [A(ns*ns) | B(ns*m)]. */
+ * nullable planner hooks (stage 1). model_params: LTI [A(ns*ns) | B(ns*m)].
+ * method 0: sequential RK4, bit-identical to the reference for polynomial
+ * models.  method 1: for linear models (single/double integrator, LTI) the
+ * RK4 step is the exact affine map s' = Phi s + Gam u and the trajectory is
+ * a parallel prefix scan (agrees to rounding); needs ws of
+ * fcb_rollout_workspace_bytes(ns) doubles; nonlinear models run method 0. */
+FCB_API size_t fcb_rollout_workspace_bytes(int ns);
 FCB_API int fcb_rollout(int model, int ns, int m, const double* model_params, const double* s0,
                 const double* U, int T, double dt, double* S, int d, const double* P,
-                double* X, int* status, int* plan_state, int iteration, fcb_stream_t stream);
+                double* X, int* status, int* plan_state, int iteration, int method,
+                double* ws, fcb_stream_t stream);
 
 /* linearize_along (dynamics.py:315-329): A (T*ns*ns), B (T*ns*m). */
 FCB_API int fcb_linearize(int model, int ns, int m, const double* model_params, const double* S,

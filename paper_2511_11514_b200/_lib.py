@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libflowcover_b200.so")
+# FCB_LIB_PATH selects an alternative build of the same library (tuning runs)
+LIB_PATH = os.environ.get("FCB_LIB_PATH") or os.path.join(_HERE, "libflowcover_b200.so")
 
 # status codes (include/flowcover_b200.h)
 FCB_OK = 0
@@ -81,7 +82,8 @@ SIGNATURES: dict[str, tuple] = {
         _I,
         [_I, _P, _I, _I, _I, _P, _D, _D, _P, _P, _P, _I, _P, _D, _P, _Z, _P],
     ),
-    "fcb_rollout": (_I, [_I, _I, _I, _P, _P, _P, _I, _D, _P, _I, _P, _P, _P, _P, _I, _P]),
+    "fcb_rollout_workspace_bytes": (_Z, [_I]),
+    "fcb_rollout": (_I, [_I, _I, _I, _P, _P, _P, _I, _D, _P, _I, _P, _P, _P, _P, _I, _I, _P, _P]),
     "fcb_linearize": (_I, [_I, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
     "fcb_lqr_workspace_bytes": (_Z, [_I, _I, _I]),
     "fcb_lqr_solve": (

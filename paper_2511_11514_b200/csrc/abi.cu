@@ -82,7 +82,8 @@ int stein_flow_full(int precision, const double* X, int n, int d, int k, const d
                     size_t ws_bytes, cudaStream_t st);
 int rollout(int model, int ns, int m, const double* prm, const double* s0, const double* U, int T,
             double dt, double* S, int d, const double* P, double* X, int* status, int* plan_state,
-            int iteration, cudaStream_t st);
+            int iteration, int method, double* ws, cudaStream_t st);
+size_t rollout_ws_bytes(int ns);
 int linearize(int model, int ns, int m, const double* prm, const double* S, const double* U, int T,
               double* A, double* B, cudaStream_t st);
 size_t lqr_ws_bytes(int ns, int m, int T);
@@ -269,12 +270,15 @@ int fcb_stein_flow_full(int precision, const double* X, int n, int d, int k,
                            plan_state, iteration, flow_log, conv_tol, ws, ws_bytes, CS(stream));
 }
 
+size_t fcb_rollout_workspace_bytes(int ns) { return rollout_ws_bytes(ns); }
+
 int fcb_rollout(int model, int ns, int m, const double* model_params, const double* s0,
                 const double* U, int T, double dt, double* S, int d, const double* P, double* X,
-                int* status, int* plan_state, int iteration, fcb_stream_t stream) {
+                int* status, int* plan_state, int iteration, int method, double* ws,
+                fcb_stream_t stream) {
     if (!(dt > 0.0)) return fail(FCB_EINPUT, "dt must be positive");
     return rollout(model, ns, m, model_params, s0, U, T, dt, S, d, P, X, status, plan_state,
-                   iteration, CS(stream));
+                   iteration, method, ws, CS(stream));
 }
 
 int fcb_linearize(int model, int ns, int m, const double* model_params, const double* S,

@@ -27,6 +27,7 @@ template <int MODEL> struct Model;
 
 template <> struct Model<FCB_MODEL_SINGLE_INTEGRATOR_2D> {
     static constexpr int N = 2, M = 2;
+    static constexpr bool LINEAR = true;
     __device__ static void f(const double* s, const double* u, const double*, double* out) {
         out[0] = u[0];
         out[1] = u[1];
@@ -39,6 +40,7 @@ template <> struct Model<FCB_MODEL_SINGLE_INTEGRATOR_2D> {
 
 template <> struct Model<FCB_MODEL_DIFF_DRIVE> {
     static constexpr int N = 3, M = 2;
+    static constexpr bool LINEAR = false;
     __device__ static void f(const double* s, const double* u, const double*, double* out) {
         out[0] = DMUL(u[0], cos(s[2]));
         out[1] = DMUL(u[0], sin(s[2]));
@@ -58,6 +60,7 @@ template <> struct Model<FCB_MODEL_DIFF_DRIVE> {
 
 template <> struct Model<FCB_MODEL_AIRCRAFT_3D> {
     static constexpr int N = 6, M = 3;
+    static constexpr bool LINEAR = false;
     __device__ static void f(const double* s, const double* u, const double*, double* out) {
         const double psi = s[3], gamma = s[4], v = s[5];
         const double cg = cos(gamma);
@@ -91,6 +94,7 @@ template <> struct Model<FCB_MODEL_AIRCRAFT_3D> {
 
 template <> struct Model<FCB_MODEL_DOUBLE_INTEGRATOR_2D> {
     static constexpr int N = 4, M = 2;
+    static constexpr bool LINEAR = true;
     __device__ static void f(const double* s, const double* u, const double*, double* out) {
         out[0] = s[2];
         out[1] = s[3];
@@ -111,6 +115,7 @@ template <> struct Model<FCB_MODEL_DOUBLE_INTEGRATOR_2D> {
 // matrix-vector products numpy would form (left-to-right dot products).
 template <int N_, int M_> struct Lti {
     static constexpr int N = N_, M = M_;
+    static constexpr bool LINEAR = true;
     __device__ static void f(const double* s, const double* u, const double* prm, double* out) {
         const double* A = prm;
         const double* B = prm + N * N;
@@ -213,6 +218,193 @@ __global__ void __launch_bounds__(32) rollout_kernel(const double* __restrict__ 
             plan_state[FCB_STATE_STAGE] = 1;
             plan_state[FCB_STATE_ITER] = iteration;
             plan_state[FCB_STATE_INDEX] = s_fail;
+        }
+    }
+}
+
+// Parallel-in-time rollout for linear models.  RK4 with zero-order hold on
+// f = A s + B u is exactly the affine map s' = Phi s + Gam u with
+//   Phi = I + hA + (hA)^2/2 + (hA)^3/6 + (hA)^4/24,
+//   Gam = h (I + hA/2 + (hA)^2/6 + (hA)^3/24) B,
+// so the trajectory is a prefix scan of affine maps (same arithmetic as the
+// RK4 stages, associated differently: results agree to rounding).  Used
+// inside the planner loop; rollout() / the final rollout stay sequential
+// and bit-exact.
+constexpr int RS_THREADS = 256;
+
+template <class Mdl>
+__global__ void __launch_bounds__(RS_THREADS) rollout_scan_kernel(
+    const double* __restrict__ prm, const double* __restrict__ s0, const double* __restrict__ U,
+    int T, double dt, double* __restrict__ S, int d, const double* __restrict__ P,
+    double* __restrict__ X, int* status, int* plan_state, int iteration, double* __restrict__ scratch) {
+    constexpr int N = Mdl::N, M = Mdl::M;
+    constexpr int ASZ = N * N + N;
+    __shared__ double sPhi[N][N], sGam[N][M], sP[3 * N];
+    __shared__ int s_fail;
+    const int tid = threadIdx.x;
+    if (plan_state && *((volatile int*)plan_state) != 0) return;
+    if (tid == 0) {
+        double A[N * N], B[N * M], z0[N] = {}, u0[M] = {};
+        Mdl::jac(z0, u0, prm, A, B);
+        double hA[N][N], Pw[N][N], Phi[N][N], Gs[N][N];
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) {
+                hA[i][j] = dt * A[i * N + j];
+                Pw[i][j] = (i == j) ? 1.0 : 0.0;
+                Phi[i][j] = Pw[i][j];
+                Gs[i][j] = Pw[i][j];
+            }
+        const double cphi[5] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0};
+        const double cgam[4] = {1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0};
+        for (int p = 1; p <= 4; ++p) {  // Pw = (hA)^p
+            double Nw[N][N];
+            for (int i = 0; i < N; ++i)
+                for (int j = 0; j < N; ++j) {
+                    double s = 0.0;
+                    for (int q = 0; q < N; ++q) s += Pw[i][q] * hA[q][j];
+                    Nw[i][j] = s;
+                }
+            for (int i = 0; i < N; ++i)
+                for (int j = 0; j < N; ++j) {
+                    Pw[i][j] = Nw[i][j];
+                    Phi[i][j] += cphi[p] * Pw[i][j];
+                    if (p <= 3) Gs[i][j] += cgam[p] * Pw[i][j];
+                }
+        }
+        for (int i = 0; i < N; ++i) {
+            for (int j = 0; j < N; ++j) sPhi[i][j] = Phi[i][j];
+            for (int j = 0; j < M; ++j) {
+                double s = 0.0;
+                for (int q = 0; q < N; ++q) s += Gs[i][q] * B[q * M + j];
+                sGam[i][j] = dt * s;
+            }
+        }
+        for (int i = 0; i < d * N; ++i) sP[i] = P ? P[i] : 0.0;
+        s_fail = 0x7fffffff;
+    }
+    __syncthreads();
+    const int L = (T + RS_THREADS - 1) / RS_THREADS;
+    const int nch = (T + L - 1) / L;
+    const int lo = tid * L, hi = min(lo + L, T);
+    double* affA = scratch;
+    double* affB = scratch + (size_t)RS_THREADS * ASZ;
+    auto input = [&](int k, double (&c)[N]) {
+        double u[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) u[j] = U[(size_t)k * M + j];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < M; ++j) s += sGam[i][j] * u[j];
+            c[i] = s;
+        }
+    };
+    if (tid < nch) {  // chunk map: Phi^L and the accumulated input response
+        Aff<N> acc;
+        aff_identity<N>(acc);
+        for (int k = lo; k < hi; ++k) {
+            double c[N], Mn[N][N], cn[N];
+            input(k, c);
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int q = 0; q < N; ++q) s += sPhi[i][q] * acc.c[q];
+                cn[i] = s + c[i];
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int q = 0; q < N; ++q) t += sPhi[i][q] * acc.M[q][j];
+                    Mn[i][j] = t;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                acc.c[i] = cn[i];
+#pragma unroll
+                for (int j = 0; j < N; ++j) acc.M[i][j] = Mn[i][j];
+            }
+        }
+        aff_store<N>(affA + (size_t)tid * ASZ, acc);
+    }
+    __syncthreads();
+    double* fs = affA;
+    double* fd = affB;
+    for (int s = 1; s < nch; s <<= 1) {
+        if (tid < nch) {
+            Aff<N> a, b, o;
+            aff_load<N>(fs + (size_t)tid * ASZ, a);
+            if (tid - s >= 0) {
+                aff_load<N>(fs + (size_t)(tid - s) * ASZ, b);
+                aff_compose<N>(a, b, o);
+                aff_store<N>(fd + (size_t)tid * ASZ, o);
+            } else {
+                aff_store<N>(fd + (size_t)tid * ASZ, a);
+            }
+        }
+        __syncthreads();
+        double* t = fs;
+        fs = fd;
+        fd = t;
+    }
+    if (tid < nch) {
+        double st[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) st[i] = s0[i];
+        if (tid > 0) {  // state at chunk start = prefix map applied to s0
+            Aff<N> pre;
+            aff_load<N>(fs + (size_t)(tid - 1) * ASZ, pre);
+            double t2[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int q = 0; q < N; ++q) s += pre.M[i][q] * st[q];
+                t2[i] = s + pre.c[i];
+            }
+#pragma unroll
+            for (int i = 0; i < N; ++i) st[i] = t2[i];
+        } else {
+#pragma unroll
+            for (int i = 0; i < N; ++i) S[i] = st[i];
+        }
+        int my_fail = 0x7fffffff;
+        for (int k = lo; k < hi; ++k) {
+            double c[N], sn[N];
+            input(k, c);
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int q = 0; q < N; ++q) s += sPhi[i][q] * st[q];
+                sn[i] = s + c[i];
+            }
+#pragma unroll
+            for (int i = 0; i < N; ++i) st[i] = sn[i];
+            if (!all_finite(st, N) && my_fail == 0x7fffffff) my_fail = k + 1;
+#pragma unroll
+            for (int i = 0; i < N; ++i) S[(size_t)(k + 1) * N + i] = st[i];
+            if (X)
+                for (int r = 0; r < d; ++r) {
+                    double a = 0.0;
+#pragma unroll
+                    for (int j = 0; j < N; ++j) a += st[j] * sP[r * N + j];
+                    X[(size_t)k * d + r] = a;
+                }
+        }
+        if (my_fail != 0x7fffffff) atomicMin(&s_fail, my_fail);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int f = (s_fail == 0x7fffffff) ? -1 : s_fail;
+        if (status) *status = f;
+        if (plan_state && f >= 0) {
+            plan_state[FCB_STATE_STOP] = 2;
+            plan_state[FCB_STATE_STAGE] = 1;
+            plan_state[FCB_STATE_ITER] = iteration;
+            plan_state[FCB_STATE_INDEX] = f;
         }
     }
 }
@@ -359,14 +551,30 @@ static int check_dims(int model, int ns, int m) {
     return FCB_OK;
 }
 
+size_t rollout_ws_bytes(int ns) {
+    return sizeof(double) * 2 * RS_THREADS * ((size_t)ns * ns + ns) + 256;
+}
+
+template <class Mdl>
+static void launch_rollout(int method, const double* prm, const double* s0, const double* U, int T,
+                           double dt, double* S, int d, const double* P, double* X, int* status,
+                           int* plan_state, int iteration, double* ws, cudaStream_t st) {
+    if (Mdl::LINEAR && method == 1 && ws != nullptr)
+        rollout_scan_kernel<Mdl><<<1, RS_THREADS, 0, st>>>(prm, s0, U, T, dt, S, d, P, X, status,
+                                                           plan_state, iteration, ws);
+    else
+        rollout_kernel<Mdl><<<1, 32, 0, st>>>(prm, s0, U, T, dt, S, d, P, X, status, plan_state,
+                                              iteration);
+}
+
 int rollout(int model, int ns, int m, const double* prm, const double* s0, const double* U, int T,
             double dt, double* S, int d, const double* P, double* X, int* status, int* plan_state,
-            int iteration, cudaStream_t st) {
+            int iteration, int method, double* ws, cudaStream_t st) {
     int rc = check_dims(model, ns, m);
     if (rc) return rc;
     if (T < 1) return fail(FCB_EINPUT, "need at least one control step");
-    FCB_MODEL_DISPATCH((rollout_kernel<Mdl><<<1, 32, 0, st>>>(prm, s0, U, T, dt, S, d, P, X, status,
-                                                              plan_state, iteration)));
+    FCB_MODEL_DISPATCH((launch_rollout<Mdl>(method, prm, s0, U, T, dt, S, d, P, X, status,
+                                            plan_state, iteration, ws, st)));
     FCB_LAUNCHED("rollout_kernel");
     return FCB_OK;
 }

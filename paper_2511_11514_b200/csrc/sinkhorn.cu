@@ -22,10 +22,14 @@
 //   a_ij = log2e * (pot_j - |x_i - y_j|^2) / w
 //        = W_j + x'_i . Yh_j + rowc_i,
 //   W_j = s (pot_j - |y'_j|^2), Yh_j = 2 s y'_j, rowc_i = -s |x'_i|^2,
-//   s = log2e / w.  A pair costs d+1 FFMA/FADD, one FMNMX, one MUFU.EX2 and
-//   one FADD: MUFU-bound (16 ex2/clk/SM).  The running max is tracked per
-//   8-column sub-tile with a lazy rescale (only when the max grows by more
-//   than 2^16), so exponents never overflow.
+//   s = log2e / w.  A pair costs d+1 FFMA/FADD, one MUFU.EX2 and one FADD:
+//   MUFU-bound (16 ex2/clk/SM).  No running max is tracked: each row is
+//   shifted by an estimate of its LSE taken from the current potential (exact
+//   at the fixed point), and an 8-column sub-tile whose partial sum leaves
+//   [2^-64, 2^64] (or is the first mass of the row) takes a rare slow path
+//   that re-shifts by the sub-tile max, so exponents never overflow.
+//   Column records are read straight from global memory (L1 broadcast,
+//   register double buffer): no shared-memory tiles, no per-tile barriers.
 // fp64 path ("direct" form, natural units): a_ij = s pot_j - s |x_i-y_j|^2,
 //   used for the reference's tight-tolerance known-answer tests.
 #include "fcb_internal.cuh"
@@ -35,6 +39,17 @@
 #include <vector>
 
 namespace fcb {
+
+// Tuning knobs (compile-time; see scripts/tune_ot.sh)
+#ifndef FCB_SMEM_TILE
+#define FCB_SMEM_TILE 1  // stage column records through shared memory
+#endif
+#ifndef FCB_TILE
+#define FCB_TILE 512     // columns per shared-memory tile
+#endif
+#ifndef FCB_MINB
+#define FCB_MINB 2       // min resident CTAs per SM (register budget)
+#endif
 
 constexpr int OT_BLOCK = 256;
 constexpr int OT_TILE = 256;    // columns staged per shared-memory tile
@@ -155,113 +170,154 @@ __global__ void omega_final_kernel(const double* __restrict__ partX, const doubl
 // ---------------------------------------------------------------------------
 template <typename Real>
 __device__ __forceinline__ double dexpu(double x) {
-    if constexpr (sizeof(Real) == 4) return exp2(x);
+    // merge-phase rescale factors: the float path only needs float accuracy
+    if constexpr (sizeof(Real) == 4) return (double)ex2_approx((float)x);
     else return exp(x);
 }
 
+// Per-row shift estimate for a sweep, from the current potential of the
+// row's own point set: at the Sinkhorn fixed point the row LSE equals
+// log(a) - pot_i / w exactly (sinkhorn.py:14-15), so shifting by it keeps
+// every term near 2^0 and the running max is never tracked.
+struct ShiftEst {
+    const double* pot;  // nullable: no estimate (shift 0, slow path fixes it)
+    double logw;        // log a (rows X) or log b (rows Y)
+    double inv_w;       // 1 / omega
+    double unit;        // exponent units per natural unit
+    __device__ __forceinline__ double at(int i) const {
+        return pot ? unit * (logw - __ldcg(pot + i) * inv_w) : 0.0;
+    }
+};
+
+template <typename Real>
+__device__ __forceinline__ Vec4<Real> load_col(const Vec4<Real>* p) {
+    // L1-cacheable broadcast load (every lane of the warp reads the same
+    // record).  Columns rewritten by other CTAs are only read after a grid
+    // barrier, whose gpu-scope fence makes them visible.
+    return *p;
+}
+
+// One work item: RPT rows per thread x columns [c0, c1) (c1 - c0 a multiple
+// of OT_SUB).  Emits the partial (shift, sum[, moments]) of every row.
 template <typename Real, int D, int RPT, bool EXP, bool BARY>
 __device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, int nrows, int row0,
                                            const Vec4<Real>* __restrict__ cols, int c0, int c1,
-                                           Real s, double* __restrict__ pm, Real* __restrict__ ps,
-                                           Real* __restrict__ pa, int ldp, int chunk,
-                                           Vec4<Real>* tile) {
+                                           Real s, const ShiftEst& est, double* __restrict__ pm,
+                                           Real* __restrict__ ps, Real* __restrict__ pa, int ldp,
+                                           int chunk) {
     using U = Units<Real>;
     const int tid = threadIdx.x;
-    const Real NEG_INF = -INFINITY;
-    const Real THRESH = 16;
-    Real x[RPT][D], rowc[RPT], rc[RPT], sum[RPT], acc[RPT][D];
+    const Real BIG = (sizeof(Real) == 4) ? Real(1.8446744e19) : Real(1e150);   // 2^64
+    const Real TINY = (sizeof(Real) == 4) ? Real(5.421011e-20) : Real(1e-150); // 2^-64
+    Real x[RPT][D], rc[RPT], sum[RPT], acc[RPT][D];
+    double rowc_d[RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
-        int i = min(row0 + r * OT_BLOCK + tid, nrows - 1);
+        const int i = min(row0 + r * OT_BLOCK + tid, nrows - 1);
         const Real* rp = reinterpret_cast<const Real*>(rows + i);
-        Vec4<Real> v{__ldcg(rp), __ldcg(rp + 1), __ldcg(rp + 2), __ldcg(rp + 3)};
+        const Vec4<Real> v{__ldcg(rp), __ldcg(rp + 1), __ldcg(rp + 2), __ldcg(rp + 3)};
 #pragma unroll
         for (int k = 0; k < D; ++k) x[r][k] = vget(v, k);
-        rowc[r] = EXP ? v.w : Real(0);
-        rc[r] = rowc[r];
+        rowc_d[r] = EXP ? (double)v.w : 0.0;
+        rc[r] = (Real)(rowc_d[r] - est.at(i));
         sum[r] = 0;
 #pragma unroll
         for (int k = 0; k < D; ++k) acc[r][k] = 0;
     }
-    for (int t0 = c0; t0 < c1; t0 += OT_TILE) {
-        const int len = min(OT_TILE, c1 - t0);
-        __syncthreads();
-        for (int k = tid; k < len; k += OT_BLOCK) {
-            Vec4<Real> v;
-            const Real* src = reinterpret_cast<const Real*>(cols + t0 + k);
-            v.x = __ldcg(src + 0);
-            v.y = __ldcg(src + 1);
-            v.z = __ldcg(src + 2);
-            v.w = __ldcg(src + 3);
-            tile[k] = v;
+#if FCB_SMEM_TILE
+    // columns staged through shared memory (coalesced cooperative loads,
+    // LDS.128 broadcast reads)
+    __shared__ Vec4<Real> s_tile[FCB_TILE];
+    for (int t0 = c0; t0 < c1; t0 += FCB_TILE) {
+    const int tlen = min(FCB_TILE, c1 - t0);
+    __syncthreads();
+    for (int k = tid; k < tlen; k += OT_BLOCK) s_tile[k] = load_col(cols + t0 + k);
+    __syncthreads();
+    for (int c = 0; c < tlen; c += OT_SUB) {
+        Real cy[OT_SUB][D], cw[OT_SUB];
+#pragma unroll
+        for (int k = 0; k < OT_SUB; ++k) {
+            const Vec4<Real> v = s_tile[c + k];
+#pragma unroll
+            for (int q = 0; q < D; ++q) cy[k][q] = vget(v, q);
+            cw[k] = v.w;
         }
-        __syncthreads();
-        for (int c = 0; c < len; c += OT_SUB) {
-            Real cy[OT_SUB][D], cw[OT_SUB];
+#else
+    // register double buffer of column records
+    Vec4<Real> nxt[OT_SUB];
+#pragma unroll
+    for (int k = 0; k < OT_SUB; ++k) nxt[k] = load_col(cols + c0 + k);
+    {
+    for (int c = c0; c < c1; c += OT_SUB) {
+        Real cy[OT_SUB][D], cw[OT_SUB];
+#pragma unroll
+        for (int k = 0; k < OT_SUB; ++k) {
+#pragma unroll
+            for (int q = 0; q < D; ++q) cy[k][q] = vget(nxt[k], q);
+            cw[k] = nxt[k].w;
+        }
+        if (c + OT_SUB < c1) {
+#pragma unroll
+            for (int k = 0; k < OT_SUB; ++k) nxt[k] = load_col(cols + c + OT_SUB + k);
+        }
+#endif
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            Real t[OT_SUB], e[OT_SUB];
 #pragma unroll
             for (int k = 0; k < OT_SUB; ++k) {
-                Vec4<Real> v = tile[c + k];
+                if constexpr (EXP) {
+                    Real a = cw[k] + rc[r];
 #pragma unroll
-                for (int q = 0; q < D; ++q) cy[k][q] = vget(v, q);
-                cw[k] = v.w;
-            }
+                    for (int q = 0; q < D; ++q) a = fma(x[r][q], cy[k][q], a);
+                    t[k] = a;
+                } else {
+                    Real d2 = 0;
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                Real t[OT_SUB];
-#pragma unroll
-                for (int k = 0; k < OT_SUB; ++k) {
-                    if constexpr (EXP) {
-                        Real a = cw[k] + rc[r];
-#pragma unroll
-                        for (int q = 0; q < D; ++q) a = fma(x[r][q], cy[k][q], a);
-                        t[k] = a;
-                    } else {
-                        Real d2 = 0;
-#pragma unroll
-                        for (int q = 0; q < D; ++q) {
-                            Real df = x[r][q] - cy[k][q];
-                            d2 = fma(df, df, d2);
-                        }
-                        t[k] = fma(-s, d2, cw[k] + rc[r]);
+                    for (int q = 0; q < D; ++q) {
+                        const Real df = x[r][q] - cy[k][q];
+                        d2 = fma(df, df, d2);
                     }
+                    t[k] = fma(-s, d2, cw[k] + rc[r]);
                 }
+                e[k] = U::expu(t[k]);
+            }
+            Real ts = ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
+            if (!(ts <= BIG) || !(sum[r] + ts >= TINY)) {
+                // slow path (rare): overflow, NaN, or nothing accumulated yet
+                // and the shift estimate is far above this row's terms
                 Real mx = t[0];
 #pragma unroll
                 for (int k = 1; k < OT_SUB; ++k) mx = fmax(mx, t[k]);
-                if ((mx > THRESH || !(sum[r] > Real(0))) && mx > NEG_INF) {
+                if (mx > Real(-INFINITY)) {
                     const Real sc = (sum[r] > Real(0)) ? U::expu(-mx) : Real(0);
                     sum[r] *= sc;
 #pragma unroll
                     for (int q = 0; q < D; ++q) acc[r][q] *= sc;
                     rc[r] -= mx;
 #pragma unroll
-                    for (int k = 0; k < OT_SUB; ++k) t[k] -= mx;
+                    for (int k = 0; k < OT_SUB; ++k) e[k] = U::expu(t[k] - mx);
+                    ts = ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
                 }
-                Real ts = 0, ta[D];
+            }
+            sum[r] += ts;
+            if constexpr (BARY) {
 #pragma unroll
-                for (int q = 0; q < D; ++q) ta[q] = 0;
+                for (int q = 0; q < D; ++q) {
+                    Real ta = 0;
 #pragma unroll
-                for (int k = 0; k < OT_SUB; ++k) {
-                    const Real e = U::expu(t[k]);
-                    ts += e;
-                    if constexpr (BARY) {
-#pragma unroll
-                        for (int q = 0; q < D; ++q) ta[q] = fma(e, cy[k][q], ta[q]);
-                    }
-                }
-                sum[r] += ts;
-                if constexpr (BARY) {
-#pragma unroll
-                    for (int q = 0; q < D; ++q) acc[r][q] += ta[q];
+                    for (int k = 0; k < OT_SUB; ++k) ta = fma(e[k], cy[k][q], ta);
+                    acc[r][q] += ta;
                 }
             }
         }
     }
+    }  // tile loop (FCB_SMEM_TILE) / buffer scope
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
         const int i = row0 + r * OT_BLOCK + tid;
         if (i < nrows) {
-            pm[(size_t)chunk * ldp + i] = (double)rowc[r] - (double)rc[r];
+            pm[(size_t)chunk * ldp + i] = rowc_d[r] - (double)rc[r];
             ps[(size_t)chunk * ldp + i] = sum[r];
             if constexpr (BARY) {
 #pragma unroll
@@ -273,16 +329,16 @@ __device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, 
 
 template <typename Real, int D, int RPT, bool EXP, bool BARY>
 __device__ __forceinline__ void run_sweep(const Sweep& sw, const Vec4<Real>* rows,
-                                          const Vec4<Real>* cols, Real s, double* pm, Real* ps,
-                                          Real* pa, Vec4<Real>* tile) {
+                                          const Vec4<Real>* cols, Real s, const ShiftEst& est,
+                                          double* pm, Real* ps, Real* pa) {
     const int ldp = sw.rows;
     for (int item = blockIdx.x; item < sw.items; item += gridDim.x) {
         const int rb = item % sw.nrb;
         const int ch = item / sw.nrb;
         const int c0 = ch * sw.chunk_len;
         const int c1 = min(c0 + sw.chunk_len, sw.cols8);
-        sweep_item<Real, D, RPT, EXP, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT, cols, c0, c1, s, pm,
-                                            ps, pa, ldp, ch, tile);
+        sweep_item<Real, D, RPT, EXP, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT, cols, c0, c1, s, est,
+                                            pm, ps, pa, ldp, ch);
     }
 }
 
@@ -381,10 +437,8 @@ __device__ __forceinline__ void merge_phase(const Sweep& sw, const double* pm, c
 // the persistent solver
 // ---------------------------------------------------------------------------
 template <typename Real, int D, int RPT, bool BARY>
-__global__ void __launch_bounds__(OT_BLOCK) ot_solve_kernel(OtArgs<Real> p) {
+__global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Real> p) {
     constexpr bool EXP = (sizeof(Real) == 4);
-    extern __shared__ __align__(32) unsigned char smem_raw[];
-    Vec4<Real>* tile = reinterpret_cast<Vec4<Real>*>(smem_raw);
     __shared__ double red[32];
 
     if (p.gate && *((volatile const int*)p.gate) != 0) return;
@@ -448,8 +502,10 @@ __global__ void __launch_bounds__(OT_BLOCK) ot_solve_kernel(OtArgs<Real> p) {
     }
     grid_sync(p.bar);
 
+    const double unit = Units<Real>::unit;
     if (sweep_only) {
-        run_sweep<Real, D, RPT, EXP, false>(p.B, p.rowX, p.colY, s, p.pm, p.ps, p.pa, tile);
+        const ShiftEst none{nullptr, 0.0, 0.0, unit};
+        run_sweep<Real, D, RPT, EXP, false>(p.B, p.rowX, p.colY, s, none, p.pm, p.ps, p.pa);
         grid_sync(p.bar);
         double* out = p.f_out;
         merge_phase<Real, D, false>(p.B, p.pm, p.ps, p.pa,
@@ -467,7 +523,9 @@ __global__ void __launch_bounds__(OT_BLOCK) ot_solve_kernel(OtArgs<Real> p) {
         unsigned long long* slot = p.errslot + (it % 3);
         if (asym) {
             // ---- sweep A: rows Y, columns X (potential f) --------------
-            run_sweep<Real, D, RPT, EXP, false>(p.A, p.rowY, p.colX, s, p.pm, p.ps, p.pa, tile);
+            // shift estimate: g of the previous iteration (none at it == 1)
+            const ShiftEst estA{it > 1 ? p.gbuf : nullptr, p.logb, 1.0 / w, unit};
+            run_sweep<Real, D, RPT, EXP, false>(p.A, p.rowY, p.colX, s, estA, p.pm, p.ps, p.pa);
             grid_sync(p.bar);
             // ---- merge A: g = w (log b - Lg) ---------------------------
             merge_phase<Real, D, false>(p.A, p.pm, p.ps, p.pa, [&](int j, double L, const double*) {
@@ -478,8 +536,9 @@ __global__ void __launch_bounds__(OT_BLOCK) ot_solve_kernel(OtArgs<Real> p) {
             grid_sync(p.bar);
         }
         // ---- sweep B: rows X, columns Y (ASYM, potential g) or X (SYM) --
-        run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, asym ? p.colY : p.colX, s, p.pm, p.ps,
-                                           p.pa, tile);
+        const ShiftEst estB{fcur, p.loga, 1.0 / w, unit};
+        run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, asym ? p.colY : p.colX, s, estB, p.pm, p.ps,
+                                           p.pa);
         grid_sync(p.bar);
         // ---- merge B ------------------------------------------------------
         double emax = 0.0;
@@ -574,13 +633,14 @@ static int ot_grid_size(int* grid) {
     static int cached = -1;
     if (cached < 0) {
         int per_sm = 0;
-        const size_t smem = OT_TILE * sizeof(Vec4<Real>);
-        FCB_CUDA(cudaFuncSetAttribute(ot_solve_kernel<Real, D, RPT, BARY>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, ot_solve_kernel<Real, D, RPT, BARY>, OT_BLOCK, smem));
+            &per_sm, ot_solve_kernel<Real, D, RPT, BARY>, OT_BLOCK, 0));
         if (per_sm < 1) return fail(FCB_ECUDA, "ot_solve_kernel cannot be resident");
-        per_sm = std::min(per_sm, 2);
+        // more resident CTAs hide MUFU/FMA latency but add grid-barrier
+        // arrivals; FCB_OT_CTAS_PER_SM overrides the default of 2
+        int cap = 2;
+        if (const char* env = getenv("FCB_OT_CTAS_PER_SM")) cap = std::max(1, atoi(env));
+        per_sm = std::min(per_sm, cap);
         cached = per_sm * sm_count();
     }
     *grid = cached;
@@ -652,9 +712,8 @@ static int ot_launch(int mode, const double* X, int n, const double* Y, int m, c
     a.gate = gate;
     FCB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(GridBarrier), st));
     void* args[] = {&a};
-    const size_t smem = OT_TILE * sizeof(Vec4<Real>);
     FCB_CUDA(cudaLaunchCooperativeKernel((const void*)ot_solve_kernel<Real, D, RPT, BARY>,
-                                         dim3(grid), dim3(OT_BLOCK), args, smem, st));
+                                         dim3(grid), dim3(OT_BLOCK), args, 0, st));
     FCB_LAUNCHED("ot_solve_kernel");
     return FCB_OK;
 }

@@ -285,6 +285,7 @@ def plan_detailed(
         flow_ws = _dev.Workspace.get(lib.fcb_stein_flow_full_workspace_bytes(prec, T, d), "plan_flow")
         log_np1 = math.log(T + 1.0)
     upd_ws = _dev.Workspace.get(lib.fcb_plan_update_workspace_bytes(n_s, m_c, T), "plan_upd")
+    roll_ws = _dev.Workspace.get(lib.fcb_rollout_workspace_bytes(n_s), "plan_roll")
     if want_metric:
         Ym = np.atleast_2d(np.asarray(q_metric, dtype=np.float64))
         Mm = Ym.shape[0]
@@ -310,7 +311,7 @@ def plan_detailed(
         e0.record()
         call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0),
              _dev.ptr(Ubuf[cur]), T, float(disc.dt), _dev.ptr(Sbuf[cur]), d, _dev.ptr(P),
-             _dev.ptr(X), None, state_ptr, it, stream)
+             _dev.ptr(X), None, state_ptr, it, 1, _dev.ptr(roll_ws), stream)
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
         if want_metric and it % cfg.metric_interval == 0:
@@ -400,7 +401,7 @@ def plan_detailed(
     S_final = _dev.zeros((T + 1, n_s), device=dev)
     call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0), _dev.ptr(U_final),
          T, float(disc.dt), _dev.ptr(S_final), d, _dev.ptr(P), _dev.ptr(X), _dev.ptr(status),
-         None, 0, stream)
+         None, 0, 0, None, stream)
     ef1 = torch.cuda.Event(enable_timing=True)
     ef1.record()
     ef1.synchronize()
