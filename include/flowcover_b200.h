@@ -107,7 +107,9 @@ FCB_API int fcb_resolve_omega(int mode, const double* X, int n, const double* Y,
  * bary     : nullable (n*(d+1)): per row the unclipped plan row mass and
  *            plan barycentre, i.e. sum_j T_ij and sum_j T_ij y_j / sum_j T_ij
  *            at the returned potentials (feeds the transport gradient,
- *            sinkhorn.py:383-391).  */
+ *            sinkhorn.py:383-391).  In SWEEP mode: {1, weighted mean of
+ *            the columns under the sweep's softmax weights} per row, which
+ *            is what an M-sharded caller needs to combine shards. */
 FCB_API size_t fcb_ot_workspace_bytes(int mode, int precision, int n, int m, int d);
 FCB_API int fcb_ot_solve(int mode, int precision, const double* X, int n, const double* Y, int m, int d,
                  const double* scal, int max_iters, double tol, const double* f0,

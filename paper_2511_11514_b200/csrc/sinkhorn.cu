@@ -505,11 +505,18 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
     const double unit = Units<Real>::unit;
     if (sweep_only) {
         const ShiftEst none{nullptr, 0.0, 0.0, unit};
-        run_sweep<Real, D, RPT, EXP, false>(p.B, p.rowX, p.colY, s, none, p.pm, p.ps, p.pa);
+        run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, p.colY, s, none, p.pm, p.ps, p.pa);
         grid_sync(p.bar);
         double* out = p.f_out;
-        merge_phase<Real, D, false>(p.B, p.pm, p.ps, p.pa,
-                                    [&](int i, double L, const double*) { out[i] = L; });
+        double* bo = p.bary;
+        merge_phase<Real, D, BARY>(p.B, p.pm, p.ps, p.pa, [&](int i, double L, const double* bar) {
+            out[i] = L;
+            if (BARY && bo) {  // weighted mean of the columns (M-shard combine)
+                double* o = bo + (size_t)i * (D + 1);
+                o[0] = 1.0;
+                for (int q = 0; q < D; ++q) o[1 + q] = bar[q] / csc + c[q];
+            }
+        });
         return;
     }
 

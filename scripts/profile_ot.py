@@ -89,5 +89,27 @@ if __name__ == "__main__":
         phases()
     elif what == "solve":
         solve()
-    else:
+    elif what == "sweep":
         sweep(int(sys.argv[2]), int(sys.argv[3]))
+
+
+def lqr(T=2000, reps=5):
+    rng = np.random.default_rng(0)
+    n, m = 4, 2
+    A = np.zeros((T, n, n)); A[:, 0, 2] = A[:, 1, 3] = 1.0
+    B = np.zeros((T, n, m)); B[:, 2, 0] = B[:, 3, 1] = 1.0
+    P = np.zeros((2, 4)); P[0, 0] = P[1, 1] = 1.0
+    a = rng.normal(size=(T, 2)) @ P
+    sys_ = fc.LtvSystem(A=A, B=B, dt=0.05)
+    w = fc.workspace_weights(P, 2)
+    for _ in range(reps):
+        fc.solve_flow_lqr(sys_, a, w)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fc.solve_flow_lqr(sys_, a, w)
+    print(f"lqr T={T}: {(time.perf_counter()-t0)/reps*1e3:.3f} ms per solve (incl. host copies)")
+
+
+if __name__ == "__main__" and sys.argv[1] == "lqr":
+    lqr(int(sys.argv[2]) if len(sys.argv) > 2 else 2000)
