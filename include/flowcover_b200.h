@@ -200,9 +200,9 @@ FCB_API int fcb_stein_flow_full(int precision, const double* X, int n, int d, in
  * method 0: sequential RK4, bit-identical to the reference for polynomial
  * models.  method 1: for linear models (single/double integrator, LTI) the
  * RK4 step is the exact affine map s' = Phi s + Gam u and the trajectory is
- * a parallel prefix scan (agrees to rounding); needs ws of
- * fcb_rollout_workspace_bytes(ns) doubles; nonlinear models run method 0. */
-FCB_API size_t fcb_rollout_workspace_bytes(int ns);
+ * a parallel prefix scan (agrees to rounding); needs a workspace of
+ * fcb_rollout_workspace_bytes(ns, T) bytes; nonlinear models run method 0. */
+FCB_API size_t fcb_rollout_workspace_bytes(int ns, int T);
 FCB_API int fcb_rollout(int model, int ns, int m, const double* model_params, const double* s0,
                 const double* U, int T, double dt, double* S, int d, const double* P,
                 double* X, int* status, int* plan_state, int iteration, int method,
@@ -225,12 +225,18 @@ FCB_API size_t fcb_lqr_workspace_bytes(int ns, int m, int T);
 /* One planner update (optimizer.py:259-268): linearize along (S, U) on the
  * fly, lift the workspace flow (lqr.py:140-142), solve the flow LQR and
  * write U_next = clamp(U + eta * v*).  lqr_costs[iteration] gets the cost;
- * a Riccati blow-up marks plan_state failed (stage 3).  clamp nullable. */
+ * a Riccati blow-up marks plan_state failed (stage 3).  clamp nullable.
+ * The LQR runs in two phases (csrc/lqr_split.cuh): a flow-independent
+ * Riccati scan (gains, closed-loop maps) and a per-flow affine phase.
+ * mode 0 runs both; mode 1 runs only the affine phase and reuses the Riccati
+ * outputs left in `ws` by an earlier mode-0 call -- valid when the model's
+ * Jacobians are state-independent (single/double integrator, LTI), whose
+ * Riccati inputs are then bitwise identical. */
 FCB_API int fcb_plan_update(int model, int ns, int m, const double* model_params, const double* S,
                     const double* U, int T, double dt, int d, const double* P,
                     const double* flow, const double* Q, const double* R, double eta,
                     const double* clamp, double* U_next, double* lqr_costs, int* plan_state,
-                    int iteration, double* ws, size_t ws_bytes, fcb_stream_t stream);
+                    int iteration, int mode, double* ws, size_t ws_bytes, fcb_stream_t stream);
 FCB_API size_t fcb_plan_update_workspace_bytes(int ns, int m, int T);
 
 /* ---- measurement helpers ------------------------------------------------- */

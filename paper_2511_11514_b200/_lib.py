@@ -82,7 +82,7 @@ SIGNATURES: dict[str, tuple] = {
         _I,
         [_I, _P, _I, _I, _I, _P, _D, _D, _P, _P, _P, _I, _P, _D, _P, _Z, _P],
     ),
-    "fcb_rollout_workspace_bytes": (_Z, [_I]),
+    "fcb_rollout_workspace_bytes": (_Z, [_I, _I]),
     "fcb_rollout": (_I, [_I, _I, _I, _P, _P, _P, _I, _D, _P, _I, _P, _P, _P, _P, _I, _I, _P, _P]),
     "fcb_linearize": (_I, [_I, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
     "fcb_lqr_workspace_bytes": (_Z, [_I, _I, _I]),
@@ -93,7 +93,8 @@ SIGNATURES: dict[str, tuple] = {
     "fcb_plan_update_workspace_bytes": (_Z, [_I, _I, _I]),
     "fcb_plan_update": (
         _I,
-        [_I, _I, _I, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _I, _P, _Z, _P],
+        [_I, _I, _I, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _I, _I, _P, _Z,
+         _P],
     ),
     "fcb_peak_probe": (_I, [_I, _I, _P, _P]),
 }

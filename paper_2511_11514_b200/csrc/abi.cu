@@ -83,7 +83,7 @@ int stein_flow_full(int precision, const double* X, int n, int d, int k, const d
 int rollout(int model, int ns, int m, const double* prm, const double* s0, const double* U, int T,
             double dt, double* S, int d, const double* P, double* X, int* status, int* plan_state,
             int iteration, int method, double* ws, cudaStream_t st);
-size_t rollout_ws_bytes(int ns);
+size_t rollout_ws_bytes(int ns, int T);
 int linearize(int model, int ns, int m, const double* prm, const double* S, const double* U, int T,
               double* A, double* B, cudaStream_t st);
 size_t lqr_ws_bytes(int ns, int m, int T);
@@ -94,7 +94,8 @@ size_t plan_update_ws_bytes(int ns, int m, int T);
 int plan_update(int model, int ns, int m, const double* prm, const double* S, const double* U,
                 int T, double dt, int d, const double* P, const double* flow, const double* Q,
                 const double* R, double eta, const double* clamp, double* Unext, double* lqr_costs,
-                int* plan_state, int iteration, double* ws, size_t ws_bytes, cudaStream_t st);
+                int* plan_state, int iteration, int mode, double* ws, size_t ws_bytes,
+                cudaStream_t st);
 
 // ---- peak probe: MUFU.EX2 and FFMA throughput -----------------------------
 constexpr int PROBE_BLOCK = 256;
@@ -270,7 +271,7 @@ int fcb_stein_flow_full(int precision, const double* X, int n, int d, int k,
                            plan_state, iteration, flow_log, conv_tol, ws, ws_bytes, CS(stream));
 }
 
-size_t fcb_rollout_workspace_bytes(int ns) { return rollout_ws_bytes(ns); }
+size_t fcb_rollout_workspace_bytes(int ns, int T) { return rollout_ws_bytes(ns, T); }
 
 int fcb_rollout(int model, int ns, int m, const double* model_params, const double* s0,
                 const double* U, int T, double dt, double* S, int d, const double* P, double* X,
@@ -304,9 +305,10 @@ int fcb_plan_update(int model, int ns, int m, const double* model_params, const 
                     const double* U, int T, double dt, int d, const double* P,
                     const double* flow, const double* Q, const double* R, double eta,
                     const double* clamp, double* U_next, double* lqr_costs, int* plan_state,
-                    int iteration, double* ws, size_t ws_bytes, fcb_stream_t stream) {
+                    int iteration, int mode, double* ws, size_t ws_bytes, fcb_stream_t stream) {
+    if (mode < 0 || mode > 1) return fail(FCB_EINPUT, "plan_update mode must be 0 or 1");
     return plan_update(model, ns, m, model_params, S, U, T, dt, d, P, flow, Q, R, eta, clamp,
-                       U_next, lqr_costs, plan_state, iteration, ws, ws_bytes, CS(stream));
+                       U_next, lqr_costs, plan_state, iteration, mode, ws, ws_bytes, CS(stream));
 }
 
 int fcb_peak_probe(int which, int iters, double* out, fcb_stream_t stream) {

@@ -11,6 +11,7 @@
 // one thread with its matrices in registers (n <= 6, m <= 3).
 #include "fcb_internal.cuh"
 #include "lqr_scan.cuh"
+#include "plan_scan.cuh"
 
 #include <algorithm>
 
@@ -476,23 +477,19 @@ struct LiftedFlow {
 };
 
 template <int N, int M>
-__global__ void __launch_bounds__(LQR_THREADS) lqr_solve_kernel(LqrScanArgs p, const double* A,
-                                                                 const double* B, const double* a) {
+__global__ void __launch_bounds__(LQR_THREADS) lqr_riccati_arrays_kernel(RicArgs p, const double* A,
+                                                                          const double* B) {
     ArrayJac<N, M> jac{A, B};
-    ArrayFlow<N> fl{a};
-    lqr_scan_body<N, M>(jac, fl, p);
+    riccati_body<N, M>(jac, p);
 }
 
 template <class Mdl>
-__global__ void __launch_bounds__(LQR_THREADS) plan_update_kernel(LqrScanArgs p, const double* prm,
-                                                                   const double* S, const double* U,
-                                                                   const double* flow,
-                                                                   const double* P, int d) {
-    constexpr int N = Mdl::N;
+__global__ void __launch_bounds__(LQR_THREADS) plan_riccati_kernel(RicArgs p, const double* prm,
+                                                                    const double* S,
+                                                                    const double* U) {
     if (p.plan_state && *((volatile int*)p.plan_state) != 0) return;
     ModelJac<Mdl> jac{prm, S, U};
-    LiftedFlow<N> fl{flow, P, d};
-    lqr_scan_body<N, Mdl::M>(jac, fl, p);
+    riccati_body<Mdl::N, Mdl::M>(jac, p);
 }
 
 // ---------------------------------------------------------------------------
@@ -551,20 +548,87 @@ static int check_dims(int model, int ns, int m) {
     return FCB_OK;
 }
 
-size_t rollout_ws_bytes(int ns) {
-    return sizeof(double) * 2 * RS_THREADS * ((size_t)ns * ns + ns) + 256;
+// Phi = I + hA + (hA)^2/2 + (hA)^3/6 + (hA)^4/24, Gam = h (I + hA/2 + (hA)^2/6
+// + (hA)^3/24) B: one RK4/ZOH step of a linear model as an affine map.
+template <class Mdl>
+__global__ void phigam_kernel(const double* prm, double dt, double* out, const int* gate) {
+    constexpr int N = Mdl::N, M = Mdl::M;
+    if (threadIdx.x != 0) return;
+    if (gate && *((volatile const int*)gate) != 0) return;
+    double A[N * N], B[N * M], z0[N] = {}, u0[M] = {};
+    Mdl::jac(z0, u0, prm, A, B);
+    double hA[N][N], Pw[N][N], Phi[N][N], Gs[N][N];
+    for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) {
+            hA[i][j] = dt * A[i * N + j];
+            Pw[i][j] = Phi[i][j] = Gs[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+    const double cphi[5] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0};
+    const double cgam[4] = {1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0};
+    for (int p = 1; p <= 4; ++p) {
+        double Nw[N][N];
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) {
+                double s = 0.0;
+                for (int q = 0; q < N; ++q) s += Pw[i][q] * hA[q][j];
+                Nw[i][j] = s;
+            }
+        for (int i = 0; i < N; ++i)
+            for (int j = 0; j < N; ++j) {
+                Pw[i][j] = Nw[i][j];
+                Phi[i][j] += cphi[p] * Pw[i][j];
+                if (p <= 3) Gs[i][j] += cgam[p] * Pw[i][j];
+            }
+    }
+    for (int i = 0; i < N; ++i) {
+        for (int j = 0; j < N; ++j) out[i * N + j] = Phi[i][j];
+        for (int j = 0; j < M; ++j) {
+            double s = 0.0;
+            for (int q = 0; q < N; ++q) s += Gs[i][q] * B[q * M + j];
+            out[N * N + i * M + j] = dt * s;
+        }
+    }
 }
 
+struct RollWs {
+    double* phigam;
+    double* scan;
+    int* first_bad;
+    size_t bytes;
+};
+
+static RollWs roll_layout(int ns, int T, void* ws) {
+    Arena ar(ws, ws ? (size_t)-1 : 0);
+    RollWs L{};
+    L.phigam = ar.take<double>(6 * 6 + 6 * 3);
+    L.scan = ar.take<double>(affscan_scratch_doubles<6>(T));  // sized for the largest N
+    L.first_bad = ar.take<int>(4);
+    L.bytes = ar.off + 256;
+    (void)ns;
+    return L;
+}
+
+size_t rollout_ws_bytes(int ns, int T) { return roll_layout(ns, T, nullptr).bytes; }
+
 template <class Mdl>
-static void launch_rollout(int method, const double* prm, const double* s0, const double* U, int T,
-                           double dt, double* S, int d, const double* P, double* X, int* status,
-                           int* plan_state, int iteration, double* ws, cudaStream_t st) {
-    if (Mdl::LINEAR && method == 1 && ws != nullptr)
-        rollout_scan_kernel<Mdl><<<1, RS_THREADS, 0, st>>>(prm, s0, U, T, dt, S, d, P, X, status,
-                                                           plan_state, iteration, ws);
-    else
-        rollout_kernel<Mdl><<<1, 32, 0, st>>>(prm, s0, U, T, dt, S, d, P, X, status, plan_state,
-                                              iteration);
+static int launch_rollout(int method, const double* prm, const double* s0, const double* U, int T,
+                          double dt, double* S, int d, const double* P, double* X, int* status,
+                          int* plan_state, int iteration, double* ws, cudaStream_t st) {
+    constexpr int N = Mdl::N, M = Mdl::M;
+    if (Mdl::LINEAR && method == 1 && ws != nullptr) {
+        RollWs L = roll_layout(N, T, ws);
+        cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st);
+        phigam_kernel<Mdl><<<1, 32, 0, st>>>(prm, dt, L.phigam, plan_state);
+        RollMap<N, M> mapf{L.phigam, U};
+        RollOut<N> out{S, s0, X, P, d, L.first_bad};
+        const int n = affscan_run<N, true>(T, mapf, out, s0, affscan_bufs<N>(L.scan, T),
+                                           plan_state, st);
+        roll_finish_kernel<<<1, 32, 0, st>>>(L.first_bad, status, plan_state, iteration);
+        return n + 2;
+    }
+    rollout_kernel<Mdl><<<1, 32, 0, st>>>(prm, s0, U, T, dt, S, d, P, X, status, plan_state,
+                                          iteration);
+    return 1;
 }
 
 int rollout(int model, int ns, int m, const double* prm, const double* s0, const double* U, int T,
@@ -573,8 +637,10 @@ int rollout(int model, int ns, int m, const double* prm, const double* s0, const
     int rc = check_dims(model, ns, m);
     if (rc) return rc;
     if (T < 1) return fail(FCB_EINPUT, "need at least one control step");
-    FCB_MODEL_DISPATCH((launch_rollout<Mdl>(method, prm, s0, U, T, dt, S, d, P, X, status,
-                                            plan_state, iteration, ws, st)));
+    int launches = 0;
+    FCB_MODEL_DISPATCH((launches = launch_rollout<Mdl>(method, prm, s0, U, T, dt, S, d, P, X,
+                                                       status, plan_state, iteration, ws, st)));
+    count_launch(launches - 1);
     FCB_LAUNCHED("rollout_kernel");
     return FCB_OK;
 }
@@ -590,31 +656,79 @@ int linearize(int model, int ns, int m, const double* prm, const double* S, cons
     return FCB_OK;
 }
 
-// scan scratch: ping-pong aggregates + affine maps, then K and d
-static size_t scan_scratch_doubles(int ns) {
-    const size_t esz = 3 * (size_t)ns * ns + 2 * ns;
-    const size_t asz = (size_t)ns * ns + ns;
-    return 2 * LQR_THREADS * esz + 2 * LQR_THREADS * asz;
+// Workspace of the two-phase LQR: Riccati scan aggregates, per-step Riccati
+// outputs (K, H^-1 G', Phi, Acl, G), d, the affine-scan scratch and a status
+// word.
+struct LqrWs {
+    double *agg, *K, *Lg, *Phi, *Acl, *Gm, *dff, *scan;
+    int* fail;
+    size_t bytes;
+};
+
+static LqrWs lqr_layout(int ns, int m, int T, void* ws) {
+    Arena ar(ws, ws ? (size_t)-1 : 0);
+    LqrWs L{};
+    L.agg = ar.take<double>(2 * (size_t)LQR_THREADS * 3 * ns * ns);
+    L.K = ar.take<double>((size_t)T * m * ns);
+    L.Lg = ar.take<double>((size_t)T * m * ns);
+    L.Phi = ar.take<double>((size_t)T * ns * ns);
+    L.Acl = ar.take<double>((size_t)T * ns * ns);
+    L.Gm = ar.take<double>((size_t)T * ns * m);
+    L.dff = ar.take<double>((size_t)T * m);
+    L.scan = ar.take<double>(affscan_scratch_doubles<6>(T));
+    L.fail = ar.take<int>(4);
+    L.bytes = ar.off + 256;
+    return L;
 }
 
-size_t lqr_ws_bytes(int ns, int m, int T) {
-    return sizeof(double) * (scan_scratch_doubles(ns) + (size_t)T * m * ns + (size_t)T * m) + 512;
+size_t lqr_ws_bytes(int ns, int m, int T) { return lqr_layout(ns, m, T, nullptr).bytes; }
+
+static RicArgs ric_args(const LqrWs& L, int T, double dt, const double* Q, const double* R) {
+    RicArgs r{};
+    r.T = T;
+    r.dt = dt;
+    r.Q = Q;
+    r.R = R;
+    r.agg = L.agg;
+    r.K = L.K;
+    r.Lg = L.Lg;
+    r.Phi = L.Phi;
+    r.Acl = L.Acl;
+    r.Gm = L.Gm;
+    r.fail = L.fail;
+    return r;
 }
 
-static LqrScanArgs scan_args(int ns, int m, int T, double dt, const double* Q, const double* R,
-                             double* ws) {
-    LqrScanArgs p{};
-    const size_t esz = 3 * (size_t)ns * ns + 2 * ns;
-    p.T = T;
-    p.dt = dt;
-    p.Q = Q;
-    p.R = R;
-    p.agg = ws;
-    p.aff = ws + 2 * LQR_THREADS * esz;
-    double* tail = ws + scan_scratch_doubles(ns);
-    p.K = tail;
-    p.dff = tail + (size_t)T * m * ns;
-    return p;
+// The affine phase: eta (backward scan, emits d), z (forward scan: v*, cost,
+// z, U update), then the finish kernel.  Returns the number of launches.
+template <int N, int M, class Flow>
+static int affine_phase(const LqrWs& L, const double* K, double* dff, int T, double dt,
+                        const double* Q, const double* R, const Flow& flow, double* v, double* z,
+                        const double* U, double* U_next, double eta, const double* clamp,
+                        double* cost, double* lqr_costs, int* plan_state, int iteration,
+                        cudaStream_t st) {
+    const AffScanBufs b = affscan_bufs<N>(L.scan, T);
+    EtaMap<N, Flow> emap{L.Phi, Q, dt, flow};
+    EtaOut<N, M> eout{L.Lg, dff, L.fail};
+    int n = affscan_run<N, false>(T, emap, eout, nullptr, b, plan_state, st);
+    ZMap<N, M> zmap{L.Acl, L.Gm, dff};
+    ZOut<N, M, Flow> zout{K, dff, Q, R, dt, flow, L.fail, v, z, U, U_next, eta, clamp};
+    n += affscan_run<N, true>(T, zmap, zout, nullptr, b, plan_state, st);
+    lqr_finish_kernel<<<1, 32, 0, st>>>(affscan_blocks(T), b.red, L.fail, cost, lqr_costs,
+                                        plan_state, iteration, plan_state != nullptr);
+    return n + 1;
+}
+
+template <int N, int M>
+static int lqr_solve_t(int T, double dt, const double* A, const double* B, const double* Q,
+                       const double* R, const double* a, double* v, double* z, double* K,
+                       double* dff, double* scal, const LqrWs& L, cudaStream_t st) {
+    RicArgs r = ric_args(L, T, dt, Q, R);
+    if (K) r.K = K;
+    lqr_riccati_arrays_kernel<N, M><<<1, LQR_THREADS, 0, st>>>(r, A, B);
+    ArrayFlow<N> fl{a};
+    return 1 + affine_phase<N, M>(L, r.K, dff ? dff : L.dff, T, dt, Q, R, fl, v, z, nullptr,
+                                  nullptr, 0.0, nullptr, scal, nullptr, nullptr, 0, st);
 }
 
 int lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B, const double* Q,
@@ -622,16 +736,11 @@ int lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B,
               double* scal, int* status, double* ws, cudaStream_t st) {
     if (T < 1) return fail(FCB_EINPUT, "horizon must be >= 1");
     if (!ws) return fail(FCB_EWORKSPACE, "lqr needs a workspace (fcb_lqr_workspace_bytes)");
-    LqrScanArgs p = scan_args(ns, m, T, dt, Q, R, ws);
-    if (K) p.K = K;
-    if (dff) p.dff = dff;
-    p.v = v;
-    p.z = z;
-    p.cost = scal;
-    p.fail = status;
-#define FCB_LQR_CASE(NN, MM)                                                          \
-    case NN * 4 + MM:                                                                 \
-        lqr_solve_kernel<NN, MM><<<1, LQR_THREADS, 0, st>>>(p, A, B, a);              \
+    LqrWs L = lqr_layout(ns, m, T, ws);
+    int n = 0;
+#define FCB_LQR_CASE(NN, MM)                                                                  \
+    case NN * 4 + MM:                                                                         \
+        n = lqr_solve_t<NN, MM>(T, dt, A, B, Q, R, a, v, z, K, dff, scal, L, st);             \
         break;
     switch (ns * 4 + m) {
         FCB_LQR_CASE(1, 1) FCB_LQR_CASE(1, 2) FCB_LQR_CASE(1, 3)
@@ -643,34 +752,52 @@ int lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B,
         default: return fail(FCB_ENOTSUP, "lqr needs 1<=n<=6 and 1<=m<=3");
     }
 #undef FCB_LQR_CASE
-    FCB_LAUNCHED("lqr_solve_kernel");
+    count_launch(n - 1);
+    FCB_LAUNCHED("lqr_scan_kernels");
+    FCB_CUDA(cudaMemcpyAsync(status, L.fail, sizeof(int), cudaMemcpyDeviceToDevice, st));
     return FCB_OK;
 }
 
-size_t plan_update_ws_bytes(int ns, int m, int T) { return lqr_ws_bytes(ns, m, T) + 256; }
+size_t plan_update_ws_bytes(int ns, int m, int T) { return lqr_ws_bytes(ns, m, T); }
+
+template <class Mdl>
+static int launch_plan_update(int mode, const LqrWs& L, int T, double dt, const double* Q,
+                              const double* R, const double* prm, const double* S, const double* U,
+                              const double* flow, const double* P, int d, double eta,
+                              const double* clamp, double* Unext, double* lqr_costs,
+                              int* plan_state, int iteration, cudaStream_t st) {
+    constexpr int N = Mdl::N, M = Mdl::M;
+    int n = 0;
+    if (mode != 1) {
+        RicArgs r = ric_args(L, T, dt, Q, R);
+        r.plan_state = plan_state;
+        r.iteration = iteration;
+        plan_riccati_kernel<Mdl><<<1, LQR_THREADS, 0, st>>>(r, prm, S, U);
+        n = 1;
+    } else {
+        cudaMemsetAsync(L.fail, 0xff, sizeof(int), st);  // -1: the stored Riccati phase is valid
+    }
+    LiftedFlow<N> fl{flow, P, d};
+    return n + affine_phase<N, M>(L, L.K, L.dff, T, dt, Q, R, fl, nullptr, nullptr, U, Unext, eta,
+                                  clamp, nullptr, lqr_costs, plan_state, iteration, st);
+}
 
 int plan_update(int model, int ns, int m, const double* prm, const double* S, const double* U,
                 int T, double dt, int d, const double* P, const double* flow, const double* Q,
                 const double* R, double eta, const double* clamp, double* Unext, double* lqr_costs,
-                int* plan_state, int iteration, double* ws, size_t ws_bytes, cudaStream_t st) {
+                int* plan_state, int iteration, int mode, double* ws, size_t ws_bytes,
+                cudaStream_t st) {
     int rc = check_dims(model, ns, m);
     if (rc) return rc;
     if (ws_bytes < plan_update_ws_bytes(ns, m, T))
         return fail(FCB_EWORKSPACE, "plan_update workspace too small");
-    LqrScanArgs p = scan_args(ns, m, T, dt, Q, R, ws);
-    // the status word lives after the scan scratch
-    int* fail_word = reinterpret_cast<int*>(ws + (lqr_ws_bytes(ns, m, T) - 512) / sizeof(double));
-    p.fail = fail_word;
-    p.U = U;
-    p.U_next = Unext;
-    p.eta = eta;
-    p.clamp = clamp;
-    p.lqr_costs = lqr_costs;
-    p.plan_state = plan_state;
-    p.iteration = iteration;
-    FCB_MODEL_DISPATCH((plan_update_kernel<Mdl><<<1, LQR_THREADS, 0, st>>>(p, prm, S, U, flow, P,
-                                                                           d)));
-    FCB_LAUNCHED("plan_update_kernel");
+    LqrWs L = lqr_layout(ns, m, T, ws);
+    int n = 0;
+    FCB_MODEL_DISPATCH((n = launch_plan_update<Mdl>(mode, L, T, dt, Q, R, prm, S, U, flow, P, d,
+                                                    eta, clamp, Unext, lqr_costs, plan_state,
+                                                    iteration, st)));
+    count_launch(n - 1);
+    FCB_LAUNCHED("plan_update_kernels");
     return FCB_OK;
 }
 

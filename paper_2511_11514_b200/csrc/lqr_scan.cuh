@@ -364,438 +364,6 @@ __device__ __forceinline__ void step_data(const Jac& jac, const Flow& flow, int 
     }
 }
 
-struct LqrScanArgs {
-    int T;
-    double dt;
-    const double* Q;  // N x N (weights, not yet scaled by dt)
-    const double* R;  // M x M
-    double* agg;      // 2 * THREADS * ESZ   (suffix aggregates, ping-pong)
-    double* aff;      // 2 * THREADS * (N*N+N)
-    double* K;        // T * M * N
-    double* dff;      // T * M
-    double* v;        // T * M (may be null when U_next is given)
-    double* z;        // (T+1) * N (nullable)
-    double* cost;     // nullable device scalar
-    int* fail;        // device int: -1 or the Riccati failure index
-    // planner hooks (nullable)
-    const double* U;
-    double* U_next;
-    double eta;
-    const double* clamp;
-    double* lqr_costs;
-    int* plan_state;
-    int iteration;
-};
-
-template <int N, int M, class Jac, class Flow>
-__device__ void lqr_scan_body(const Jac& jac, const Flow& flow, const LqrScanArgs& p) {
-    constexpr int ESZ = elem_doubles<N>();
-    constexpr int ASZ = N * N + N;
-    __shared__ double sQb[N][N], sRb[M][M], sRtinv[M][M];
-    __shared__ int s_fail;
-    __shared__ double s_red[32];
-    const int tid = threadIdx.x;
-    const int T = p.T;
-    const double dt = p.dt;
-    if (tid == 0) {
-        s_fail = -1;
-        for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) sQb[i][j] = dt * p.Q[i * N + j];
-        for (int i = 0; i < M; ++i)
-            for (int j = 0; j < M; ++j) sRb[i][j] = dt * p.R[i * M + j];
-        // Rt^-1 = (2 Rb)^-1 by Gauss-Jordan on the tiny m x m matrix
-        double Aa[M][2 * M];
-        for (int i = 0; i < M; ++i)
-            for (int j = 0; j < 2 * M; ++j)
-                Aa[i][j] = (j < M) ? 2.0 * sRb[i][j] : ((j - M == i) ? 1.0 : 0.0);
-        for (int c = 0; c < M; ++c) {
-            int pv = c;
-            for (int r = c + 1; r < M; ++r)
-                if (fabs(Aa[r][c]) > fabs(Aa[pv][c])) pv = r;
-            for (int k = 0; k < 2 * M; ++k) {
-                double t = Aa[c][k];
-                Aa[c][k] = Aa[pv][k];
-                Aa[pv][k] = t;
-            }
-            const double inv = 1.0 / Aa[c][c];
-            for (int k = 0; k < 2 * M; ++k) Aa[c][k] *= inv;
-            for (int r = 0; r < M; ++r)
-                if (r != c) {
-                    const double l = Aa[r][c];
-                    for (int k = 0; k < 2 * M; ++k) Aa[r][k] -= l * Aa[c][k];
-                }
-        }
-        for (int i = 0; i < M; ++i)
-            for (int j = 0; j < M; ++j) sRtinv[i][j] = Aa[i][M + j];
-    }
-    __syncthreads();
-
-    // elements 0..T (T is the zero terminal element)
-    const int total = T + 1;
-    const int L = (total + LQR_THREADS - 1) / LQR_THREADS;
-    const int nch = (total + L - 1) / L;
-    const int lo = tid * L, hi = min(lo + L, total);
-
-    auto base_elem = [&](int k, Elem<N>& e) {
-        if (k >= T) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                e.b[i] = 0.0;
-                e.h[i] = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) e.A[i][j] = e.C[i][j] = e.J[i][j] = 0.0;
-            }
-            return;
-        }
-        double F[N][N], G[N][M], ak[N];
-        step_data<N, M>(jac, flow, k, dt, F, G, ak);
-        double GR[N][M];
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int j = 0; j < M; ++j) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < M; ++q) s += G[i][q] * sRtinv[q][j];
-                GR[i][j] = s;
-            }
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            e.b[i] = 0.0;
-            double qa = 0.0;
-#pragma unroll
-            for (int q = 0; q < N; ++q) qa += sQb[i][q] * ak[q];
-            e.h[i] = 2.0 * qa;
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                e.A[i][j] = F[i][j];
-                e.J[i][j] = 2.0 * sQb[i][j];
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < M; ++q) s += GR[i][q] * G[j][q];
-                e.C[i][j] = s;
-            }
-        }
-    };
-
-    // ---- P1: chunk aggregates (suffix products inside the chunk) ---------
-    double* aggA = p.agg;
-    double* aggB = p.agg + (size_t)LQR_THREADS * ESZ;
-    if (tid < nch) {
-        Elem<N> acc, e, tmp;
-        base_elem(hi - 1, acc);
-        for (int k = hi - 2; k >= lo; --k) {
-            base_elem(k, e);
-            elem_combine<N>(e, acc, tmp);
-            acc = tmp;
-        }
-        elem_store<N>(aggA + (size_t)tid * ESZ, acc);
-    }
-    __syncthreads();
-    // ---- P2: inclusive suffix scan over the aggregates (Hillis-Steele) ---
-    double* src = aggA;
-    double* dst = aggB;
-    for (int s = 1; s < nch; s <<= 1) {
-        if (tid < nch) {
-            Elem<N> a, b, o;
-            elem_load<N>(src + (size_t)tid * ESZ, a);
-            if (tid + s < nch) {
-                elem_load<N>(src + (size_t)(tid + s) * ESZ, b);
-                elem_combine<N>(a, b, o);
-                elem_store<N>(dst + (size_t)tid * ESZ, o);
-            } else {
-                elem_store<N>(dst + (size_t)tid * ESZ, a);
-            }
-        }
-        __syncthreads();
-        double* t = src;
-        src = dst;
-        dst = t;
-    }
-    // ---- P3: information-form re-walk, gains K_k, d_k --------------------
-    if (tid < nch) {
-        double J2[N][N], h2[N];
-        if (tid + 1 < nch) {
-            const double* sp = src + (size_t)(tid + 1) * ESZ;
-#pragma unroll
-            for (int i = 0; i < N * N; ++i) (&J2[0][0])[i] = __ldcg(sp + 2 * N * N + 2 * N + i);
-#pragma unroll
-            for (int i = 0; i < N; ++i) h2[i] = __ldcg(sp + 2 * N * N + N + i);
-        } else {
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                h2[i] = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) J2[i][j] = 0.0;
-            }
-        }
-        int local_fail = -1;
-        for (int k = hi - 1; k >= lo; --k) {
-            if (k < T) {
-                // gains from the suffix k+1 (P' = J2/2, p' = -h2/2)
-                double F[N][N], G[N][M], ak[N];
-                step_data<N, M>(jac, flow, k, dt, F, G, ak);
-                double PG[N][M], PF[N][N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) {
-#pragma unroll
-                    for (int j = 0; j < M; ++j) {
-                        double s = 0.0;
-#pragma unroll
-                        for (int q = 0; q < N; ++q) s += J2[i][q] * G[q][j];
-                        PG[i][j] = 0.5 * s;
-                    }
-#pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        double s = 0.0;
-#pragma unroll
-                        for (int q = 0; q < N; ++q) s += J2[i][q] * F[q][j];
-                        PF[i][j] = 0.5 * s;
-                    }
-                }
-                double H[M][M], rhs[M][N + 1];
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-#pragma unroll
-                    for (int j = 0; j < M; ++j) {
-                        double s = 0.0;
-#pragma unroll
-                        for (int q = 0; q < N; ++q) s += G[q][i] * PG[q][j];
-                        H[i][j] = sRb[i][j] + s;
-                    }
-#pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        double s = 0.0;
-#pragma unroll
-                        for (int q = 0; q < N; ++q) s += G[q][i] * PF[q][j];
-                        rhs[i][j] = s;
-                    }
-                    double s = 0.0;
-#pragma unroll
-                    for (int q = 0; q < N; ++q) s += G[q][i] * h2[q];
-                    rhs[i][N] = 0.5 * s;  // -G' p' with p' = -h2/2
-                }
-                // H X = rhs (partial pivoting)
-#pragma unroll
-                for (int col = 0; col < M; ++col) {
-                    int pv = col;
-#pragma unroll
-                    for (int r = col + 1; r < M; ++r)
-                        if (fabs(H[r][col]) > fabs(H[pv][col])) pv = r;
-                    if (pv != col) {
-#pragma unroll
-                        for (int q = 0; q < M; ++q) {
-                            double t = H[col][q];
-                            H[col][q] = H[pv][q];
-                            H[pv][q] = t;
-                        }
-#pragma unroll
-                        for (int q = 0; q < N + 1; ++q) {
-                            double t = rhs[col][q];
-                            rhs[col][q] = rhs[pv][q];
-                            rhs[pv][q] = t;
-                        }
-                    }
-#pragma unroll
-                    for (int r = col + 1; r < M; ++r) {
-                        const double l = H[r][col] / H[col][col];
-#pragma unroll
-                        for (int q = col; q < M; ++q) H[r][q] -= l * H[col][q];
-#pragma unroll
-                        for (int q = 0; q < N + 1; ++q) rhs[r][q] -= l * rhs[col][q];
-                    }
-                }
-#pragma unroll
-                for (int r = M - 1; r >= 0; --r)
-#pragma unroll
-                    for (int q = 0; q < N + 1; ++q) {
-                        double vv = rhs[r][q];
-#pragma unroll
-                        for (int c2 = r + 1; c2 < M; ++c2) vv -= H[r][c2] * rhs[c2][q];
-                        rhs[r][q] = vv / H[r][r];
-                    }
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-#pragma unroll
-                    for (int j = 0; j < N; ++j) p.K[((size_t)k * M + i) * N + j] = rhs[i][j];
-                    p.dff[(size_t)k * M + i] = rhs[i][N];
-                }
-                // advance the suffix to k (information form)
-                Elem<N> e;
-                base_elem(k, e);
-                info_step<N>(e, J2, h2);
-                bool finite = true;
-#pragma unroll
-                for (int i = 0; i < N; ++i) {
-                    finite = finite && isfinite(h2[i]);
-#pragma unroll
-                    for (int j = 0; j < N; ++j) finite = finite && isfinite(J2[i][j]);
-                }
-                if (!finite && local_fail < 0) local_fail = k;
-            }
-        }
-        if (local_fail >= 0) atomicMax(&s_fail, local_fail);
-    }
-    __syncthreads();
-    if (s_fail >= 0) {
-        if (tid == 0) {
-            *p.fail = s_fail;
-            if (p.plan_state) {
-                p.plan_state[FCB_STATE_STOP] = 2;
-                p.plan_state[FCB_STATE_STAGE] = 3;
-                p.plan_state[FCB_STATE_ITER] = p.iteration;
-                p.plan_state[FCB_STATE_INDEX] = s_fail;
-            }
-        }
-        return;
-    }
-    // ---- P4: chunk compositions of the closed-loop maps -------------------
-    // maps for k = 0..T-1:  z_{k+1} = (F_k - G_k K_k) z_k + G_k d_k
-    const int Lf = (T + LQR_THREADS - 1) / LQR_THREADS;
-    const int nchf = (T + Lf - 1) / Lf;
-    const int flo = tid * Lf, fhi = min(flo + Lf, T);
-    auto step_map = [&](int k, Aff<N>& a) {
-        double F[N][N], G[N][M], ak[N];
-        step_data<N, M>(jac, flow, k, dt, F, G, ak);
-        double Kk[M][N], dk[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-#pragma unroll
-            for (int j = 0; j < N; ++j) Kk[i][j] = __ldcg(p.K + ((size_t)k * M + i) * N + j);
-            dk[i] = __ldcg(p.dff + (size_t)k * M + i);
-        }
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            double cc = 0.0;
-#pragma unroll
-            for (int q = 0; q < M; ++q) cc += G[i][q] * dk[q];
-            a.c[i] = cc;
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < M; ++q) s += G[i][q] * Kk[q][j];
-                a.M[i][j] = F[i][j] - s;
-            }
-        }
-    };
-    double* affA = p.aff;
-    double* affB = p.aff + (size_t)LQR_THREADS * ASZ;
-    if (tid < nchf) {
-        Aff<N> acc, m, tmp;
-        aff_identity<N>(acc);
-        for (int k = flo; k < fhi; ++k) {
-            step_map(k, m);
-            aff_compose<N>(m, acc, tmp);
-            acc = tmp;
-        }
-        aff_store<N>(affA + (size_t)tid * ASZ, acc);
-    }
-    __syncthreads();
-    // ---- P5: inclusive prefix scan over chunk maps ------------------------
-    double* fs = affA;
-    double* fd = affB;
-    for (int s = 1; s < nchf; s <<= 1) {
-        if (tid < nchf) {
-            Aff<N> a, b, o;
-            aff_load<N>(fs + (size_t)tid * ASZ, a);
-            if (tid - s >= 0) {
-                aff_load<N>(fs + (size_t)(tid - s) * ASZ, b);
-                aff_compose<N>(a, b, o);
-                aff_store<N>(fd + (size_t)tid * ASZ, o);
-            } else {
-                aff_store<N>(fd + (size_t)tid * ASZ, a);
-            }
-        }
-        __syncthreads();
-        double* t = fs;
-        fs = fd;
-        fd = t;
-    }
-    // ---- P6: re-walk: z, v*, cost, control update --------------------------
-    double cost_part = 0.0;
-    if (tid < nchf) {
-        double zz[N];
-        if (tid == 0) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) zz[i] = 0.0;
-        } else {  // z at chunk start = offset of the exclusive prefix (z_0 = 0)
-#pragma unroll
-            for (int i = 0; i < N; ++i) zz[i] = __ldcg(fs + (size_t)(tid - 1) * ASZ + N * N + i);
-        }
-        if (p.z && tid == 0)
-#pragma unroll
-            for (int i = 0; i < N; ++i) p.z[i] = 0.0;
-        for (int k = flo; k < fhi; ++k) {
-            double F[N][N], G[N][M], ak[N];
-            step_data<N, M>(jac, flow, k, dt, F, G, ak);
-            double vk[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) s += __ldcg(p.K + ((size_t)k * M + i) * N + j) * zz[j];
-                vk[i] = __ldcg(p.dff + (size_t)k * M + i) - s;
-            }
-            double e[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) e[i] = ak[i] - zz[i];
-            double c1 = 0.0, c2 = 0.0;
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) s += sQb[i][j] * e[j];
-                c1 += e[i] * s;
-            }
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < M; ++j) s += sRb[i][j] * vk[j];
-                c2 += vk[i] * s;
-            }
-            cost_part += c1 + c2;
-            if (p.v)
-#pragma unroll
-                for (int i = 0; i < M; ++i) p.v[(size_t)k * M + i] = vk[i];
-            if (p.U_next) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    double u = p.U[(size_t)k * M + i] + p.eta * vk[i];
-                    if (p.clamp) {
-                        const double b = p.clamp[i];
-                        u = fmin(fmax(u, -b), b);
-                    }
-                    p.U_next[(size_t)k * M + i] = u;
-                }
-            }
-            double zn[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) s1 += F[i][j] * zz[j];
-#pragma unroll
-                for (int j = 0; j < M; ++j) s2 += G[i][j] * vk[j];
-                zn[i] = s1 + s2;
-            }
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                zz[i] = zn[i];
-                if (p.z) p.z[(size_t)(k + 1) * N + i] = zz[i];
-            }
-        }
-    }
-    const double total_cost = block_sum<LQR_THREADS>(cost_part, s_red);
-    if (tid == 0) {
-        *p.fail = -1;
-        if (p.cost) *p.cost = total_cost;
-        if (p.plan_state) {
-            p.lqr_costs[p.iteration] = total_cost;
-            p.plan_state[FCB_STATE_UPDATES] = p.iteration + 1;
-        }
-    }
-}
-
 }  // namespace fcb
+
+#include "lqr_split.cuh"

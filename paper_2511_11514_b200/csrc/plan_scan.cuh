@@ -1,0 +1,243 @@
+// plan_scan.cuh -- the planner's per-iteration time recurrences as affine scans
+// (affscan.cuh): the linear-model rollout and the two passes of the LQR
+// affine phase (lqr_split.cuh), each with its outputs fused into the scan's
+// consumer.
+#pragma once
+
+#include "affscan.cuh"
+#include "fcb_internal.cuh"
+
+namespace fcb {
+
+// ---------------------------------------------------------------------------
+// LQR affine phase
+// ---------------------------------------------------------------------------
+// backward: eta_k = Phi_k' eta_{k+1} + 2 Qb a_k
+template <int N, class Flow>
+struct EtaMap {
+    const double* Phi;
+    const double* Q;
+    double dt;
+    Flow flow;
+    __device__ void operator()(int k, AMap<N>& m) const {
+        double ak[N];
+        flow.get(k, ak);
+        const double* Pk = Phi + (size_t)k * N * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) s += Q[i * N + q] * ak[q];
+            m.c[i] = 2.0 * dt * s;
+#pragma unroll
+            for (int j = 0; j < N; ++j) m.M[i][j] = Pk[j * N + i];
+        }
+    }
+};
+
+// consumer: d_k = 1/2 Lg_k eta_{k+1}; the first non-finite eta index
+template <int N, int M>
+struct EtaOut {
+    const double* Lg;
+    double* dff;
+    int* fail;
+    __device__ double operator()(int k, const double* e_next, const double* e_k) const {
+        const double* Lk = Lg + (size_t)k * M * N;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) s += Lk[i * N + j] * e_next[j];
+            dff[(size_t)k * M + i] = 0.5 * s;
+        }
+        bool finite = true;
+#pragma unroll
+        for (int i = 0; i < N; ++i) finite = finite && isfinite(e_k[i]);
+        if (!finite) atomicMax(fail, k);
+        return 0.0;
+    }
+};
+
+// forward: z_{k+1} = Acl_k z_k + G_k d_k
+template <int N, int M>
+struct ZMap {
+    const double* Acl;
+    const double* Gm;
+    const double* dff;
+    __device__ void operator()(int k, AMap<N>& m) const {
+        const double* Ak = Acl + (size_t)k * N * N;
+        const double* Gk = Gm + (size_t)k * N * M;
+        double dk[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) dk[i] = dff[(size_t)k * M + i];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double cc = 0.0;
+#pragma unroll
+            for (int q = 0; q < M; ++q) cc += Gk[i * M + q] * dk[q];
+            m.c[i] = cc;
+#pragma unroll
+            for (int j = 0; j < N; ++j) m.M[i][j] = Ak[i * N + j];
+        }
+    }
+};
+
+// consumer: v_k = d_k - K_k z_k, the stage cost, z, the control update
+template <int N, int M, class Flow>
+struct ZOut {
+    const double* K;
+    const double* dff;
+    const double* Q;
+    const double* R;
+    double dt;
+    Flow flow;
+    const int* fail;
+    double* v;
+    double* z;
+    const double* U;
+    double* U_next;
+    double eta;
+    const double* clamp;
+    __device__ double operator()(int k, const double* zk, const double* zk1) const {
+        if (*((volatile const int*)fail) >= 0) return 0.0;
+        const double* Kk = K + (size_t)k * M * N;
+        double vk[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) s += Kk[i * N + j] * zk[j];
+            vk[i] = dff[(size_t)k * M + i] - s;
+        }
+        double ak[N], e[N];
+        flow.get(k, ak);
+#pragma unroll
+        for (int i = 0; i < N; ++i) e[i] = ak[i] - zk[i];
+        double c1 = 0.0, c2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) s += (dt * Q[i * N + j]) * e[j];
+            c1 += e[i] * s;
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < M; ++j) s += (dt * R[i * M + j]) * vk[j];
+            c2 += vk[i] * s;
+        }
+        if (v)
+#pragma unroll
+            for (int i = 0; i < M; ++i) v[(size_t)k * M + i] = vk[i];
+        if (z) {
+            if (k == 0)
+#pragma unroll
+                for (int i = 0; i < N; ++i) z[i] = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) z[(size_t)(k + 1) * N + i] = zk1[i];
+        }
+        if (U_next)
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                double u = U[(size_t)k * M + i] + eta * vk[i];
+                if (clamp) u = fmin(fmax(u, -clamp[i]), clamp[i]);
+                U_next[(size_t)k * M + i] = u;
+            }
+        return c1 + c2;
+    }
+};
+
+// After both scans: total cost (fixed order), status, planner hooks.
+__global__ void lqr_finish_kernel(int nb, const double* red, int* fail, double* cost,
+                                  double* lqr_costs, int* plan_state, int iteration, int gated) {
+    if (threadIdx.x != 0) return;
+    if (gated && plan_state && *((volatile int*)plan_state) != 0) return;
+    const int f = *fail;
+    if (f >= 0) {
+        if (plan_state) {
+            plan_state[FCB_STATE_STOP] = 2;
+            plan_state[FCB_STATE_STAGE] = 3;
+            plan_state[FCB_STATE_ITER] = iteration;
+            plan_state[FCB_STATE_INDEX] = f;
+        }
+        return;
+    }
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += red[b];
+    if (cost) *cost = s;
+    if (plan_state) {
+        lqr_costs[iteration] = s;
+        plan_state[FCB_STATE_UPDATES] = iteration + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// linear-model rollout:  s_{k+1} = Phi s_k + Gam u_k
+// ---------------------------------------------------------------------------
+template <int N, int M>
+struct RollMap {
+    const double* PhiGam;  // [Phi (N*N) | Gam (N*M)]
+    const double* U;
+    __device__ void operator()(int k, AMap<N>& m) const {
+        double u[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) u[j] = U[(size_t)k * M + j];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < M; ++j) s += PhiGam[N * N + i * M + j] * u[j];
+            m.c[i] = s;
+#pragma unroll
+            for (int j = 0; j < N; ++j) m.M[i][j] = PhiGam[i * N + j];
+        }
+    }
+};
+
+template <int N>
+struct RollOut {
+    double* S;
+    const double* s0;
+    double* X;
+    const double* P;
+    int d;
+    int* first_bad;
+    __device__ double operator()(int k, const double* sk, const double* sk1) const {
+        if (k == 0)
+#pragma unroll
+            for (int i = 0; i < N; ++i) S[i] = s0[i];
+        bool finite = true;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            S[(size_t)(k + 1) * N + i] = sk1[i];
+            finite = finite && isfinite(sk1[i]);
+        }
+        if (X)
+            for (int r = 0; r < d; ++r) {
+                double a = 0.0;
+#pragma unroll
+                for (int j = 0; j < N; ++j) a += sk1[j] * P[r * N + j];
+                X[(size_t)k * d + r] = a;
+            }
+        if (!finite) atomicMin(first_bad, k + 1);
+        return 0.0;
+    }
+};
+
+__global__ void roll_finish_kernel(int* first_bad, int* status, int* plan_state, int iteration) {
+    if (threadIdx.x != 0) return;
+    if (plan_state && *((volatile int*)plan_state) != 0) return;
+    // first_bad starts at 0x7f7f7f7f (byte memset): no non-finite state seen
+    const int f = (*first_bad >= 0x7f7f7f7f) ? -1 : *first_bad;
+    if (status) *status = f;
+    if (plan_state && f >= 0) {
+        plan_state[FCB_STATE_STOP] = 2;
+        plan_state[FCB_STATE_STAGE] = 1;
+        plan_state[FCB_STATE_ITER] = iteration;
+        plan_state[FCB_STATE_INDEX] = f;
+    }
+}
+
+}  // namespace fcb

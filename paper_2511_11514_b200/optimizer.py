@@ -233,6 +233,9 @@ def plan_detailed(
         np.clip(U0, -bounds, bounds, out=U0)
 
     spec = device_model(model)
+    linear_model = spec.model_id in (
+        _lib.FCB_MODEL_SINGLE_INTEGRATOR_2D, _lib.FCB_MODEL_DOUBLE_INTEGRATOR_2D, _lib.FCB_MODEL_LTI
+    )
     d = model.workspace_dim
     if d > 3:
         raise NotImplementedError("device flows support workspaces of dimension 1-3")
@@ -285,7 +288,7 @@ def plan_detailed(
         flow_ws = _dev.Workspace.get(lib.fcb_stein_flow_full_workspace_bytes(prec, T, d), "plan_flow")
         log_np1 = math.log(T + 1.0)
     upd_ws = _dev.Workspace.get(lib.fcb_plan_update_workspace_bytes(n_s, m_c, T), "plan_upd")
-    roll_ws = _dev.Workspace.get(lib.fcb_rollout_workspace_bytes(n_s), "plan_roll")
+    roll_ws = _dev.Workspace.get(lib.fcb_rollout_workspace_bytes(n_s, T), "plan_roll")
     if want_metric:
         Ym = np.atleast_2d(np.asarray(q_metric, dtype=np.float64))
         Mm = Ym.shape[0]
@@ -334,11 +337,13 @@ def plan_detailed(
                  flow_ws.numel(), stream)
         e3 = torch.cuda.Event(enable_timing=True)
         e3.record()
+        # state-independent Jacobians: the Riccati phase is computed once
+        lqr_mode = 1 if (linear_model and it > 0) else 0
         call("fcb_plan_update", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(Sbuf[cur]),
              _dev.ptr(Ubuf[cur]), T, float(disc.dt), d, _dev.ptr(P), _dev.ptr(flow),
              _dev.ptr(Q), _dev.ptr(R), float(cfg.eta), _dev.ptr(clamp_d),
-             _dev.ptr(Ubuf[1 - cur]), _dev.ptr(lqr_costs), state_ptr, it, _dev.ptr(upd_ws),
-             upd_ws.numel(), stream)
+             _dev.ptr(Ubuf[1 - cur]), _dev.ptr(lqr_costs), state_ptr, it, lqr_mode,
+             _dev.ptr(upd_ws), upd_ws.numel(), stream)
         e4 = torch.cuda.Event(enable_timing=True)
         e4.record()
         marks.append((e0, e1, e2, e3, e4))
