@@ -246,6 +246,11 @@ FCB_API size_t fcb_plan_update_workspace_bytes(int ns, int m, int T);
  * the caller times the launch with events. */
 FCB_API int fcb_peak_probe(int which, int iters, double* out, fcb_stream_t stream);
 
+/* Debug builds (-DFCB_TIMELINE): globaltimer stamps of block 0 at every grid
+ * barrier of the persistent solvers, copied to a HOST array; returns the
+ * count and resets the log.  Production builds return 0. */
+FCB_API int fcb_debug_timeline(unsigned long long* host_out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

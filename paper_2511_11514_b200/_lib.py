@@ -97,6 +97,7 @@ SIGNATURES: dict[str, tuple] = {
          _P],
     ),
     "fcb_peak_probe": (_I, [_I, _I, _P, _P]),
+    "fcb_debug_timeline": (_I, [_P, _I]),
 }
 
 _lock = threading.Lock()

@@ -112,18 +112,72 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 
 // Grid-wide barrier for cooperatively launched kernels.  count/gen live in
 // the caller's workspace and start at zero.
+#ifndef FCB_HBAR
+#define FCB_HBAR 0  // 1: two-level arrival (16 group counters); measured slower
+#endif
+constexpr int HBAR_GROUPS = 16;
+
 struct GridBarrier {
     unsigned count;
     unsigned gen;
+#if FCB_HBAR
+    unsigned pad[30];
+    unsigned sub[HBAR_GROUPS * 32];  // one 128-byte line per group counter
+#endif
 };
+
+#ifdef FCB_TIMELINE
+// Debug builds only (scripts/tune_ot.sh -DFCB_TIMELINE): block 0 records the
+// globaltimer when it arrives at and leaves every grid barrier.
+__device__ unsigned long long g_timeline[8192];
+__device__ unsigned g_timeline_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define FCB_TL_MARK()                                                          \
+    do {                                                                       \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                             \
+            unsigned i_ = g_timeline_n;                                        \
+            if (i_ < 8192) g_timeline[i_] = gtimer();                          \
+            g_timeline_n = i_ + 1;                                             \
+        }                                                                      \
+    } while (0)
+#else
+#define FCB_TL_MARK() \
+    do {              \
+    } while (0)
+#endif
 
 __device__ __forceinline__ void grid_sync(GridBarrier* b) {
     __syncthreads();
+    FCB_TL_MARK();
     if (threadIdx.x == 0) {
-        unsigned nb = gridDim.x * gridDim.y * gridDim.z;
-        unsigned g = ld_acquire_u32(&b->gen);
+        const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+        const unsigned g = ld_acquire_u32(&b->gen);
         __threadfence();
-        unsigned arrived = atomicAdd(&b->count, 1u);
+#if FCB_HBAR
+        // arrivals spread over HBAR_GROUPS counters; the last CTA of each
+        // group arrives at the top counter, the last group releases
+        const unsigned ngroups = nb < (unsigned)HBAR_GROUPS ? nb : (unsigned)HBAR_GROUPS;
+        const unsigned grp = blockIdx.x % ngroups;
+        const unsigned members = nb / ngroups + (grp < nb % ngroups ? 1u : 0u);
+        bool releaser = false;
+        if (atomicAdd(&b->sub[grp * 32], 1u) == members - 1) {
+            b->sub[grp * 32] = 0;
+            __threadfence();
+            if (atomicAdd(&b->count, 1u) == ngroups - 1) {
+                b->count = 0;
+                __threadfence();
+                atomicAdd(&b->gen, 1u);
+                releaser = true;
+            }
+        }
+        if (!releaser)
+            while (ld_acquire_u32(&b->gen) == g) __nanosleep(20);
+#else
+        const unsigned arrived = atomicAdd(&b->count, 1u);
         if (arrived == nb - 1) {
             b->count = 0;
             __threadfence();
@@ -133,6 +187,31 @@ __device__ __forceinline__ void grid_sync(GridBarrier* b) {
                 __nanosleep(20);
             }
         }
+#endif
+        __threadfence();
+    }
+    __syncthreads();
+    FCB_TL_MARK();
+}
+
+// Point-to-point producer/consumer sync between CTAs of a persistent grid:
+// the producer CTA publishes an epoch after its writes; consumers spin until
+// the epoch is reached.  Epochs only grow, so flags are never reset.
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void publish_epoch(unsigned* flag, unsigned epoch) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_u32(flag, epoch);
+    }
+}
+
+__device__ __forceinline__ void wait_epoch(const unsigned* flag, unsigned epoch) {
+    if (threadIdx.x == 0) {
+        while (ld_acquire_u32(flag) < epoch) __nanosleep(32);
         __threadfence();
     }
     __syncthreads();
