@@ -29,6 +29,7 @@ template <int MODEL> struct Model;
 template <> struct Model<FCB_MODEL_SINGLE_INTEGRATOR_2D> {
     static constexpr int N = 2, M = 2;
     static constexpr bool LINEAR = true;
+    static constexpr bool TRIANGULAR = false;
     __device__ static void f(const double* s, const double* u, const double*, double* out) {
         out[0] = u[0];
         out[1] = u[1];
@@ -42,6 +43,15 @@ template <> struct Model<FCB_MODEL_SINGLE_INTEGRATOR_2D> {
 template <> struct Model<FCB_MODEL_DIFF_DRIVE> {
     static constexpr int N = 3, M = 2;
     static constexpr bool LINEAR = false;
+    // triangular structure: q = (theta) integrates u1; the position
+    // derivative depends on (q, u) only -> parallel RK4 rollout
+    static constexpr bool TRIANGULAR = true;
+    static constexpr int NQ = 1, NP = 2, QOFF = 2;
+    __device__ static void qdot(const double* u, double* qd) { qd[0] = u[1]; }
+    __device__ static void pdot(const double* q, const double* u, double* pd) {
+        pd[0] = DMUL(u[0], cos(q[0]));
+        pd[1] = DMUL(u[0], sin(q[0]));
+    }
     __device__ static void f(const double* s, const double* u, const double*, double* out) {
         out[0] = DMUL(u[0], cos(s[2]));
         out[1] = DMUL(u[0], sin(s[2]));
@@ -62,6 +72,20 @@ template <> struct Model<FCB_MODEL_DIFF_DRIVE> {
 template <> struct Model<FCB_MODEL_AIRCRAFT_3D> {
     static constexpr int N = 6, M = 3;
     static constexpr bool LINEAR = false;
+    // q = (psi, gamma, v) integrates u; positions depend on q only
+    static constexpr bool TRIANGULAR = true;
+    static constexpr int NQ = 3, NP = 3, QOFF = 3;
+    __device__ static void qdot(const double* u, double* qd) {
+        qd[0] = u[0];
+        qd[1] = u[1];
+        qd[2] = u[2];
+    }
+    __device__ static void pdot(const double* q, const double*, double* pd) {
+        const double vcg = DMUL(q[2], cos(q[1]));
+        pd[0] = DMUL(vcg, cos(q[0]));
+        pd[1] = DMUL(vcg, sin(q[0]));
+        pd[2] = DMUL(q[2], sin(q[1]));
+    }
     __device__ static void f(const double* s, const double* u, const double*, double* out) {
         const double psi = s[3], gamma = s[4], v = s[5];
         const double cg = cos(gamma);
@@ -96,6 +120,7 @@ template <> struct Model<FCB_MODEL_AIRCRAFT_3D> {
 template <> struct Model<FCB_MODEL_DOUBLE_INTEGRATOR_2D> {
     static constexpr int N = 4, M = 2;
     static constexpr bool LINEAR = true;
+    static constexpr bool TRIANGULAR = false;
     __device__ static void f(const double* s, const double* u, const double*, double* out) {
         out[0] = s[2];
         out[1] = s[3];
@@ -117,6 +142,7 @@ template <> struct Model<FCB_MODEL_DOUBLE_INTEGRATOR_2D> {
 template <int N_, int M_> struct Lti {
     static constexpr int N = N_, M = M_;
     static constexpr bool LINEAR = true;
+    static constexpr bool TRIANGULAR = false;
     __device__ static void f(const double* s, const double* u, const double* prm, double* out) {
         const double* A = prm;
         const double* B = prm + N * N;
@@ -593,6 +619,7 @@ __global__ void phigam_kernel(const double* prm, double dt, double* out, const i
 struct RollWs {
     double* phigam;
     double* scan;
+    double* dp;
     int* first_bad;
     size_t bytes;
 };
@@ -602,6 +629,7 @@ static RollWs roll_layout(int ns, int T, void* ws) {
     RollWs L{};
     L.phigam = ar.take<double>(6 * 6 + 6 * 3);
     L.scan = ar.take<double>(affscan_scratch_doubles<6>(T));  // sized for the largest N
+    L.dp = ar.take<double>((size_t)T * 3);                    // triangular models' increments
     L.first_bad = ar.take<int>(4);
     L.bytes = ar.off + 256;
     (void)ns;
@@ -620,11 +648,27 @@ static int launch_rollout(int method, const double* prm, const double* s0, const
         cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st);
         phigam_kernel<Mdl><<<1, 32, 0, st>>>(prm, dt, L.phigam, plan_state);
         RollMap<N, M> mapf{L.phigam, U};
-        RollOut<N> out{S, s0, X, P, d, L.first_bad};
+        RollOut<Mdl> out{S, s0, X, P, d, L.first_bad, prm, U, dt};
         const int n = affscan_run<N, true>(T, mapf, out, s0, affscan_bufs<N>(L.scan, T),
                                            plan_state, st);
         roll_finish_kernel<<<1, 32, 0, st>>>(L.first_bad, status, plan_state, iteration);
         return n + 2;
+    }
+    if constexpr (Mdl::TRIANGULAR) {
+        if (method == 1 && ws != nullptr) {
+            RollWs L = roll_layout(N, T, ws);
+            cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st);
+            TriQMap<Mdl> qmap{U, dt};
+            TriQOut<Mdl> qout{U, dt, S, s0, L.dp, L.first_bad};
+            int n = affscan_run<Mdl::NQ, true>(T, qmap, qout, s0 + Mdl::QOFF,
+                                               affscan_bufs<Mdl::NQ>(L.scan, T), plan_state, st);
+            TriPMap<Mdl> pmap{L.dp};
+            TriPOut<Mdl> pout{S, X, P, d, L.first_bad};
+            n += affscan_run<Mdl::NP, true>(T, pmap, pout, s0, affscan_bufs<Mdl::NP>(L.scan, T),
+                                            plan_state, st);
+            roll_finish_kernel<<<1, 32, 0, st>>>(L.first_bad, status, plan_state, iteration);
+            return n + 1;
+        }
     }
     rollout_kernel<Mdl><<<1, 32, 0, st>>>(prm, s0, U, T, dt, S, d, P, X, status, plan_state,
                                           iteration);

@@ -196,14 +196,18 @@ struct RollMap {
     }
 };
 
-template <int N>
+template <class Mdl>
 struct RollOut {
+    static constexpr int N = Mdl::N;
     double* S;
     const double* s0;
     double* X;
     const double* P;
     int d;
     int* first_bad;
+    const double* prm;
+    const double* U;
+    double dt;
     __device__ double operator()(int k, const double* sk, const double* sk1) const {
         if (k == 0)
 #pragma unroll
@@ -214,6 +218,29 @@ struct RollOut {
             S[(size_t)(k + 1) * N + i] = sk1[i];
             finite = finite && isfinite(sk1[i]);
         }
+        {
+            // the reference's step from s_k, stage by stage: an overflow in an
+            // intermediate stage marks the same step the sequential RK4 does
+            double u[Mdl::M], k1[N], k2[N], k3[N], k4[N], t[N];
+#pragma unroll
+            for (int j = 0; j < Mdl::M; ++j) u[j] = U[(size_t)k * Mdl::M + j];
+            const double half = __dmul_rn(0.5, dt), sixth = dt / 6.0;
+            Mdl::f(sk, u, prm, k1);
+#pragma unroll
+            for (int j = 0; j < N; ++j) t[j] = __dadd_rn(sk[j], __dmul_rn(half, k1[j]));
+            Mdl::f(t, u, prm, k2);
+#pragma unroll
+            for (int j = 0; j < N; ++j) t[j] = __dadd_rn(sk[j], __dmul_rn(half, k2[j]));
+            Mdl::f(t, u, prm, k3);
+#pragma unroll
+            for (int j = 0; j < N; ++j) t[j] = __dadd_rn(sk[j], __dmul_rn(dt, k3[j]));
+            Mdl::f(t, u, prm, k4);
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double inner = __dadd_rn(__dadd_rn(k1[j], __dmul_rn(2.0, __dadd_rn(k2[j], k3[j]))), k4[j]);
+                finite = finite && isfinite(__dadd_rn(sk[j], __dmul_rn(sixth, inner)));
+            }
+        }
         if (X)
             for (int r = 0; r < d; ++r) {
                 double a = 0.0;
@@ -221,6 +248,137 @@ struct RollOut {
                 for (int j = 0; j < N; ++j) a += sk1[j] * P[r * N + j];
                 X[(size_t)k * d + r] = a;
             }
+        if (!finite) atomicMin(first_bad, k + 1);
+        return 0.0;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// triangular models (diff_drive, aircraft_3d): the integrator states q obey
+// q' = qdot(u) and the positions p' = pdot(q, u), so one RK4/ZOH step is
+//   q_{k+1} = q_k + dt/6 (qd + 2 (qd + qd) + qd)
+//   p_{k+1} = p_k + dt/6 (k1 + 2 (k2 + k3) + k4),  k_i = pdot(q at stage i)
+// with stage values of q known in closed form.  Exact RK4 stage arithmetic
+// (the reference's operation order per step); only the accumulation over
+// steps is a prefix sum.
+// ---------------------------------------------------------------------------
+template <class Mdl>
+__device__ __forceinline__ void tri_qinc(const double* u, double dt, double* dq) {
+    double qd[Mdl::NQ];
+    Mdl::qdot(u, qd);
+    const double sixth = dt / 6.0;
+#pragma unroll
+    for (int i = 0; i < Mdl::NQ; ++i) {
+        const double inner = __dadd_rn(__dadd_rn(qd[i], __dmul_rn(2.0, __dadd_rn(qd[i], qd[i]))), qd[i]);
+        dq[i] = __dmul_rn(sixth, inner);
+    }
+}
+
+template <class Mdl>
+__device__ __forceinline__ void tri_pinc(const double* q, const double* u, double dt, double* dp) {
+    constexpr int NQ = Mdl::NQ, NP = Mdl::NP;
+    double qd[NQ], qs[NQ], k1[NP], k2[NP], k3[NP], k4[NP];
+    Mdl::qdot(u, qd);
+    const double half = __dmul_rn(0.5, dt), sixth = dt / 6.0;
+    Mdl::pdot(q, u, k1);
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) qs[i] = __dadd_rn(q[i], __dmul_rn(half, qd[i]));
+    Mdl::pdot(qs, u, k2);
+    Mdl::pdot(qs, u, k3);  // k3's q stage equals k2's (qd is constant over the step)
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) qs[i] = __dadd_rn(q[i], __dmul_rn(dt, qd[i]));
+    Mdl::pdot(qs, u, k4);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        const double inner = __dadd_rn(__dadd_rn(k1[i], __dmul_rn(2.0, __dadd_rn(k2[i], k3[i]))), k4[i]);
+        dp[i] = __dmul_rn(sixth, inner);
+    }
+}
+
+template <class Mdl>
+struct TriQMap {
+    const double* U;
+    double dt;
+    __device__ void operator()(int k, AMap<Mdl::NQ>& m) const {
+        double u[Mdl::M];
+#pragma unroll
+        for (int j = 0; j < Mdl::M; ++j) u[j] = U[(size_t)k * Mdl::M + j];
+        tri_qinc<Mdl>(u, dt, m.c);
+#pragma unroll
+        for (int i = 0; i < Mdl::NQ; ++i)
+#pragma unroll
+            for (int j = 0; j < Mdl::NQ; ++j) m.M[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+};
+
+// consumer of the q scan: q into S, the position increment into dp
+template <class Mdl>
+struct TriQOut {
+    const double* U;
+    double dt;
+    double* S;
+    const double* s0;
+    double* dp;  // T x NP
+    int* first_bad;
+    __device__ double operator()(int k, const double* qk, const double* qk1) const {
+        constexpr int N = Mdl::N;
+        if (k == 0)
+            for (int i = 0; i < N; ++i) S[i] = s0[i];
+        double u[Mdl::M];
+#pragma unroll
+        for (int j = 0; j < Mdl::M; ++j) u[j] = U[(size_t)k * Mdl::M + j];
+        tri_pinc<Mdl>(qk, u, dt, dp + (size_t)k * Mdl::NP);
+        bool finite = true;
+#pragma unroll
+        for (int i = 0; i < Mdl::NQ; ++i) {
+            S[(size_t)(k + 1) * N + Mdl::QOFF + i] = qk1[i];
+            finite = finite && isfinite(qk1[i]);
+        }
+        if (!finite) atomicMin(first_bad, k + 1);
+        return 0.0;
+    }
+};
+
+template <class Mdl>
+struct TriPMap {
+    const double* dp;
+    __device__ void operator()(int k, AMap<Mdl::NP>& m) const {
+#pragma unroll
+        for (int i = 0; i < Mdl::NP; ++i) {
+            m.c[i] = dp[(size_t)k * Mdl::NP + i];
+#pragma unroll
+            for (int j = 0; j < Mdl::NP; ++j) m.M[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+    }
+};
+
+// consumer of the p scan: positions into S, the workspace projection into X
+template <class Mdl>
+struct TriPOut {
+    double* S;
+    double* X;
+    const double* P;
+    int d;
+    int* first_bad;
+    __device__ double operator()(int k, const double*, const double* pk1) const {
+        constexpr int N = Mdl::N;
+        bool finite = true;
+#pragma unroll
+        for (int i = 0; i < Mdl::NP; ++i) {
+            S[(size_t)(k + 1) * N + i] = pk1[i];
+            finite = finite && isfinite(pk1[i]);
+        }
+        if (X) {
+            // X = P s_{k+1}; read the q part written by the q scan
+            for (int r = 0; r < d; ++r) {
+                double a = 0.0;
+                for (int j = 0; j < N; ++j) {
+                    const double sj = (j < Mdl::NP) ? pk1[j] : S[(size_t)(k + 1) * N + j];
+                    a += sj * P[r * N + j];
+                }
+                X[(size_t)k * d + r] = a;
+            }
+        }
         if (!finite) atomicMin(first_bad, k + 1);
         return 0.0;
     }

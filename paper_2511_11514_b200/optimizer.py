@@ -29,6 +29,7 @@ from .dynamics import (
     Trajectory,
     device_model,
     rollout,
+    rollout_method,
 )
 from .lqr import RiccatiDivergenceError, workspace_weights
 from .reference import GaussianMixture, ReferenceDistribution, SamplePoints, to_sample_based
@@ -406,7 +407,7 @@ def plan_detailed(
     S_final = _dev.zeros((T + 1, n_s), device=dev)
     call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0), _dev.ptr(U_final),
          T, float(disc.dt), _dev.ptr(S_final), d, _dev.ptr(P), _dev.ptr(X), _dev.ptr(status),
-         None, 0, 0, None, stream)
+         None, 0, rollout_method(T), _dev.ptr(roll_ws), stream)
     ef1 = torch.cuda.Event(enable_timing=True)
     ef1.record()
     ef1.synchronize()
