@@ -117,64 +117,99 @@ struct OtArgs {
 constexpr int ST_BLOCK = 256;
 constexpr int ST_GRID = 148;
 
-// per-block partial sums of a point set: [sum_d x_d, sum |x|^2] (4 doubles)
-__global__ void __launch_bounds__(ST_BLOCK) point_stats_kernel(const double* __restrict__ P, int n,
-                                                              int d, double* __restrict__ part) {
+// Both point sets in one launch: blocks [0, gx) cover X, [gx, gx + gy) Y.
+__global__ void __launch_bounds__(ST_BLOCK) pair_stats_kernel(const double* __restrict__ X, int n,
+                                                             const double* __restrict__ Y, int m,
+                                                             int d, int gx, double* __restrict__ part) {
     __shared__ double scratch[32];
+    const bool isY = (int)blockIdx.x >= gx;
+    const double* P = isY ? Y : X;
+    const int cnt = isY ? m : n;
+    const int nb = isY ? (int)gridDim.x - gx : gx;
+    const int b = isY ? (int)blockIdx.x - gx : (int)blockIdx.x;
     double acc[4] = {0, 0, 0, 0};
-    const int per = (n + gridDim.x - 1) / gridDim.x;
-    const int lo = blockIdx.x * per, hi = min(n, lo + per);
+    const int per = (cnt + nb - 1) / nb;
+    const int lo = b * per, hi = min(cnt, lo + per);
     for (int i = lo + threadIdx.x; i < hi; i += ST_BLOCK) {
         double sq = 0.0;
         for (int k = 0; k < d; ++k) {
-            double v = P[(size_t)i * d + k];
+            const double v = P[(size_t)i * d + k];
             acc[k] += v;
             sq += v * v;
         }
         acc[3] += sq;
     }
     for (int k = 0; k < 4; ++k) {
-        double r = block_sum<ST_BLOCK>(acc[k], scratch);
+        const double r = block_sum<ST_BLOCK>(acc[k], scratch);
         if (threadIdx.x == 0) part[blockIdx.x * 4 + k] = r;
     }
 }
 
-__global__ void omega_final_kernel(const double* __restrict__ partX, const double* __restrict__ partY,
-                                   int nblk, int n, int m, int d, int mode, double omega_fixed,
-                                   double unit, double* __restrict__ scal) {
-    if (threadIdx.x != 0) return;
-    double sx[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
-    for (int b = 0; b < nblk; ++b)
-        for (int k = 0; k < 4; ++k) {
-            sx[k] += partX[b * 4 + k];
-            if (partY) sy[k] += partY[b * 4 + k];
+// omega + centring (resolve_omega, sinkhorn.py:136-148), optionally the
+// self-term scal (centre = mean X) and the warm-start selection of
+// sinkhorn_flow (sinkhorn.py:364, :371), in one block.  Fixed-order sums.
+constexpr int PREP_BLOCK = 1024;
+__global__ void __launch_bounds__(PREP_BLOCK)
+    flow_prep_kernel(const double* __restrict__ part, int gx, int gy, int n, int m, int d, int mode,
+                     double omega_fixed, double unit, double* __restrict__ scal,
+                     double* __restrict__ scal_self, const double* __restrict__ warm_f,
+                     const double* __restrict__ warm_p, const int* __restrict__ warm_valid,
+                     double* __restrict__ f0, double* __restrict__ p0, unsigned* zero_count) {
+    __shared__ double scratch[32];
+    __shared__ double sums[8];
+    for (int k = 0; k < 8; ++k) {
+        const int base = (k < 4) ? 0 : gx;
+        const int cnt = (k < 4) ? gx : gy;
+        double a = 0.0;
+        for (int b = threadIdx.x; b < cnt; b += PREP_BLOCK) a += part[(base + b) * 4 + (k & 3)];
+        a = block_sum<PREP_BLOCK>(a, scratch);
+        if (threadIdx.x == 0) sums[k] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const bool haveY = gy > 0;
+        double mx[3] = {0, 0, 0}, my[3] = {0, 0, 0};
+        for (int k = 0; k < d; ++k) {
+            mx[k] = sums[k] / n;
+            my[k] = haveY ? sums[4 + k] / m : mx[k];
         }
-    double mx[3] = {0, 0, 0}, my[3] = {0, 0, 0};
-    for (int k = 0; k < d; ++k) {
-        mx[k] = sx[k] / n;
-        my[k] = partY ? sy[k] / m : mx[k];
+        const double mx2 = sums[3] / n;
+        const double my2 = haveY ? sums[7] / m : mx2;
+        double dot = 0.0;
+        for (int k = 0; k < d; ++k) dot += mx[k] * my[k];
+        double w = omega_fixed;
+        if (!(omega_fixed > 0.0)) {
+            w = AUTO_OMEGA_FACTOR * (mx2 + my2 - 2.0 * dot);
+            if (!(w >= OMEGA_FLOOR)) w = (w != w) ? w : OMEGA_FLOOR;
+        }
+        scal[SC_OMEGA] = w;
+        scal[SC_S] = unit / w;
+        for (int k = 0; k < 3; ++k) {
+            double c = 0.0;
+            if (k < d) c = (mode == FCB_OT_SYM) ? mx[k] : 0.5 * (mx[k] + my[k]);
+            scal[SC_C + k] = c;
+            scal[SC_MX + k] = mx[k];
+            scal[SC_MY + k] = my[k];
+        }
+        scal[SC_MX2] = mx2;
+        scal[SC_MY2] = my2;
+        if (zero_count) *zero_count = 0u;
+        if (scal_self) {
+            for (int k = 0; k < 16; ++k) scal_self[k] = scal[k];
+            for (int k = 0; k < 3; ++k) scal_self[SC_C + k] = (k < d) ? mx[k] : 0.0;
+        }
     }
-    const double mx2 = sx[3] / n;
-    const double my2 = partY ? sy[3] / m : mx2;
-    double dot = 0.0;
-    for (int k = 0; k < d; ++k) dot += mx[k] * my[k];
-    double w = omega_fixed;
-    if (!(omega_fixed > 0.0)) {
-        w = AUTO_OMEGA_FACTOR * (mx2 + my2 - 2.0 * dot);
-        if (!(w >= OMEGA_FLOOR)) w = (w != w) ? w : OMEGA_FLOOR;
+    if (f0) {
+        const bool vf = warm_valid && warm_valid[0] != 0;
+        const bool vp = warm_valid && warm_valid[1] != 0;
+        for (int i = threadIdx.x; i < n; i += PREP_BLOCK) {
+            f0[i] = vf ? warm_f[i] : 0.0;
+            p0[i] = vp ? warm_p[i] : 0.0;
+        }
     }
-    scal[SC_OMEGA] = w;
-    scal[SC_S] = unit / w;
-    for (int k = 0; k < 3; ++k) {
-        double c = 0.0;
-        if (k < d) c = (mode == FCB_OT_SYM) ? mx[k] : 0.5 * (mx[k] + my[k]);
-        scal[SC_C + k] = c;
-        scal[SC_MX + k] = mx[k];
-        scal[SC_MY + k] = my[k];
-    }
-    scal[SC_MX2] = mx2;
-    scal[SC_MY2] = my2;
 }
+
+static int stats_blocks(int cnt) { return std::max(1, std::min(ST_GRID, (cnt + 4 * ST_BLOCK - 1) / (4 * ST_BLOCK))); }
 
 // ---------------------------------------------------------------------------
 // sweep: one work item = (row block, column chunk)
@@ -994,27 +1029,32 @@ size_t omega_ws_bytes(int n, int m) {
     return 2 * ST_GRID * 4 * sizeof(double) + 512;
 }
 
+// Two launches: pair statistics, then omega/centring (+ optional self-term
+// scal and warm-start selection for sinkhorn_flow).
+static int omega_prep(int mode, const double* X, int n, const double* Y, int m, int d,
+                      double omega_fixed, double unit, double* scal, double* scal_self,
+                      const double* warm_f, const double* warm_p, const int* warm_valid,
+                      double* f0, double* p0, unsigned* zero_count, void* ws, size_t ws_bytes,
+                      cudaStream_t st) {
+    if (ws_bytes < omega_ws_bytes(n, m)) return fail(FCB_EWORKSPACE, "omega workspace too small");
+    double* part = static_cast<double*>(ws);
+    const bool haveY = (mode == FCB_OT_ASYM || mode == FCB_OT_SWEEP) && Y != nullptr && m > 0;
+    const int gx = stats_blocks(n);
+    const int gy = haveY ? stats_blocks(m) : 0;
+    pair_stats_kernel<<<gx + gy, ST_BLOCK, 0, st>>>(X, n, Y, m, d, gx, part);
+    FCB_LAUNCHED("pair_stats_kernel");
+    flow_prep_kernel<<<1, PREP_BLOCK, 0, st>>>(part, gx, gy, n, m, d, mode, omega_fixed, unit, scal,
+                                               scal_self, warm_f, warm_p, warm_valid, f0, p0,
+                                               zero_count);
+    FCB_LAUNCHED("flow_prep_kernel");
+    return FCB_OK;
+}
+
 int resolve_omega(int mode, const double* X, int n, const double* Y, int m, int d,
                   double omega_fixed, double unit, double* scal, void* ws, size_t ws_bytes,
                   cudaStream_t st) {
-    if (ws_bytes < omega_ws_bytes(n, m)) return fail(FCB_EWORKSPACE, "omega workspace too small");
-    double* partX = static_cast<double*>(ws);
-    double* partY = partX + ST_GRID * 4;
-    const int gx = std::max(1, std::min(ST_GRID, (n + ST_BLOCK - 1) / ST_BLOCK));
-    const bool haveY = (mode == FCB_OT_ASYM || mode == FCB_OT_SWEEP) && Y != nullptr && m > 0;
-    const int gy = haveY ? std::max(1, std::min(ST_GRID, (m + ST_BLOCK - 1) / ST_BLOCK)) : 0;
-    // both partial arrays must be combined over the same block count
-    const int g = std::max(gx, gy);
-    point_stats_kernel<<<g, ST_BLOCK, 0, st>>>(X, n, d, partX);
-    FCB_LAUNCHED("point_stats_kernel");
-    if (haveY) {
-        point_stats_kernel<<<g, ST_BLOCK, 0, st>>>(Y, m, d, partY);
-        FCB_LAUNCHED("point_stats_kernel");
-    }
-    omega_final_kernel<<<1, 32, 0, st>>>(partX, haveY ? partY : nullptr, g, n, m, d, mode,
-                                         omega_fixed, unit, scal);
-    FCB_LAUNCHED("omega_final_kernel");
-    return FCB_OK;
+    return omega_prep(mode, X, n, Y, m, d, omega_fixed, unit, scal, nullptr, nullptr, nullptr,
+                      nullptr, nullptr, nullptr, nullptr, ws, ws_bytes, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -1051,8 +1091,11 @@ __global__ void ot_plan_kernel(const double* __restrict__ X, int n, const double
 }
 
 // finalize of sinkhorn_flow: FlowError test, envelope gradient, warm state,
-// mean magnitude and the planner's convergence hook.
-constexpr int FIN_BLOCK = 1024;
+// mean magnitude and the planner's convergence hook.  Multi-block; the last
+// block to finish sums the per-block magnitudes in block order (deterministic)
+// and runs the scalar epilogue.
+constexpr int FIN_BLOCK = 256;
+constexpr int FIN_GRID = 148;
 __global__ void __launch_bounds__(FIN_BLOCK)
     flow_finalize_kernel(const double* __restrict__ X, int n, int d, double tol,
                          const double* __restrict__ rs_x, const double* __restrict__ bary_x,
@@ -1061,18 +1104,16 @@ __global__ void __launch_bounds__(FIN_BLOCK)
                          const double* __restrict__ f, const double* __restrict__ pp,
                          double* warm_f, double* warm_p, int* warm_valid, double* flow,
                          double* fstat, const double* scal, int* plan_state, int iteration,
-                         double* flow_log, double conv_tol) {
+                         double* flow_log, double conv_tol, double* part, unsigned* count) {
     __shared__ double scratch[32];
-    __shared__ int s_fail;
+    __shared__ bool s_last;
     if (plan_state && *((volatile int*)plan_state) != 0) return;
     const double ex = stat_x[0], ep = stat_p[0];
     const double worst = (ex > ep || ex != ex) ? ex : ep;
     const bool flow_error = worst > 100.0 * tol;
-    if (threadIdx.x == 0) s_fail = flow_error ? 1 : 0;
-    __syncthreads();
     double norm_acc = 0.0;
-    if (!s_fail) {
-        for (int i = threadIdx.x; i < n; i += FIN_BLOCK) {
+    if (!flow_error) {
+        for (int i = blockIdx.x * FIN_BLOCK + threadIdx.x; i < n; i += gridDim.x * FIN_BLOCK) {
             const double rcx = rs_x[i], rux = bary_x[(size_t)i * (d + 1)];
             const double rcp = rs_p[i], rup = bary_p[(size_t)i * (d + 1)];
             double sq = 0.0;
@@ -1091,8 +1132,20 @@ __global__ void __launch_bounds__(FIN_BLOCK)
             }
         }
     }
-    const double total = block_sum<FIN_BLOCK>(norm_acc, scratch);
+    const double blk = block_sum<FIN_BLOCK>(norm_acc, scratch);
     if (threadIdx.x == 0) {
+        part[blockIdx.x] = blk;
+        __threadfence();
+        s_last = atomicAdd(count, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double a = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += FIN_BLOCK) a += __ldcg(part + b);
+    const double total = block_sum<FIN_BLOCK>(a, scratch);
+    if (threadIdx.x == 0) {
+        *count = 0u;
         const double mean_mag = total / n;
         fstat[0] = worst;
         fstat[1] = (stat_x[2] != 0.0 && stat_p[2] != 0.0) ? 1.0 : 0.0;
@@ -1125,14 +1178,6 @@ __global__ void __launch_bounds__(FIN_BLOCK)
     }
 }
 
-// warm start selection: f0 = warm_f if valid else NULL -> emulate with a copy
-__global__ void warm_select_kernel(const double* warm, const int* valid, int which, int n,
-                                   double* out) {
-    const bool v = valid && valid[which] != 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        out[i] = v ? warm[i] : 0.0;
-}
-
 __global__ void divergence_combine_kernel(const double* costs, double* out) {
     if (threadIdx.x == 0) {
         out[1] = costs[0];
@@ -1157,6 +1202,8 @@ struct FlowWs {
     double *f, *g, *rs_x, *stat_x, *bary_x;
     double *p, *rs_p, *stat_p, *bary_p;
     double *f0, *p0;
+    double* fin_part;
+    unsigned* fin_count;
     void* ot_ws;
     size_t ot_bytes;
     size_t total;
@@ -1179,6 +1226,8 @@ static FlowWs flow_layout(int precision, int n, int m, int d, void* ws, size_t b
     L.bary_p = ar.take<double>((size_t)n * (d + 1));
     L.f0 = ar.take<double>(n);
     L.p0 = ar.take<double>(n);
+    L.fin_part = ar.take<double>(FIN_GRID);
+    L.fin_count = ar.take<unsigned>(4);
     L.ot_bytes = std::max(ot_ws_bytes(FCB_OT_ASYM, precision, n, m, d),
                           ot_ws_bytes(FCB_OT_SYM, precision, n, n, d));
     L.ot_ws = ar.take<char>(L.ot_bytes);
@@ -1199,34 +1248,26 @@ int sinkhorn_flow(int precision, const double* X, int n, const double* Y, int m,
                   cudaStream_t st) {
     FlowWs L = flow_layout(precision, n, m, d, ws, ws_bytes);
     if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "sinkhorn_flow workspace too small");
-    int rc = resolve_omega(FCB_OT_ASYM, X, n, Y, m, d, omega_fixed, unit_for(precision), L.scal,
-                           L.omega_ws, omega_ws_bytes(n, m), st);
+    // omega, both centrings (the self term shares omega but is centred on X)
+    // and the warm-start selection in two launches
+    const bool warm = warm_f && warm_valid;
+    const double* f0 = warm ? L.f0 : nullptr;
+    const double* p0 = warm ? L.p0 : nullptr;
+    int rc = omega_prep(FCB_OT_ASYM, X, n, Y, m, d, omega_fixed, unit_for(precision), L.scal,
+                        L.scal_self, warm_f, warm_p, warm_valid, warm ? L.f0 : nullptr,
+                        warm ? L.p0 : nullptr, L.fin_count, L.omega_ws, omega_ws_bytes(n, m), st);
     if (rc) return rc;
-    const double* f0 = nullptr;
-    const double* p0 = nullptr;
-    if (warm_f && warm_valid) {
-        warm_select_kernel<<<std::min(148, (n + 255) / 256), 256, 0, st>>>(warm_f, warm_valid, 0, n,
-                                                                           L.f0);
-        FCB_LAUNCHED("warm_select_kernel");
-        warm_select_kernel<<<std::min(148, (n + 255) / 256), 256, 0, st>>>(warm_p, warm_valid, 1, n,
-                                                                           L.p0);
-        FCB_LAUNCHED("warm_select_kernel");
-        f0 = L.f0;
-        p0 = L.p0;
-    }
     rc = ot_solve(FCB_OT_ASYM, precision, X, n, Y, m, d, L.scal, max_iters, tol, f0, L.f, L.g,
                   L.rs_x, L.stat_x, L.bary_x, plan_state, L.ot_ws, L.ot_bytes, st);
     if (rc) return rc;
-    // the self term shares omega but is centred on X
-    copy_scal_kernel<<<1, 32, 0, st>>>(L.scal, L.scal_self, L.scal + SC_MX, d);
-    FCB_LAUNCHED("copy_scal_kernel");
     rc = ot_solve(FCB_OT_SYM, precision, X, n, nullptr, 0, d, L.scal_self, max_iters, tol, p0, L.p,
                   nullptr, L.rs_p, L.stat_p, L.bary_p, plan_state, L.ot_ws, L.ot_bytes, st);
     if (rc) return rc;
-    flow_finalize_kernel<<<1, FIN_BLOCK, 0, st>>>(X, n, d, tol, L.rs_x, L.bary_x, L.stat_x, L.rs_p,
-                                                  L.bary_p, L.stat_p, L.f, L.p, warm_f, warm_p,
-                                                  warm_valid, flow, fstat, L.scal, plan_state,
-                                                  iteration, flow_log, conv_tol);
+    const int fin_grid = std::max(1, std::min(FIN_GRID, (n + 2 * FIN_BLOCK - 1) / (2 * FIN_BLOCK)));
+    flow_finalize_kernel<<<fin_grid, FIN_BLOCK, 0, st>>>(
+        X, n, d, tol, L.rs_x, L.bary_x, L.stat_x, L.rs_p, L.bary_p, L.stat_p, L.f, L.p, warm_f,
+        warm_p, warm_valid, flow, fstat, L.scal, plan_state, iteration, flow_log, conv_tol,
+        L.fin_part, L.fin_count);
     FCB_LAUNCHED("flow_finalize_kernel");
     return FCB_OK;
 }
