@@ -280,4 +280,280 @@ inline int affscan_run(int T, const MapFn& mapf, const OutFn& out, const double*
     return 3;
 }
 
+// ---------------------------------------------------------------------------
+// One-launch scans for horizons up to AS_BLK * AS_BLK steps (fused_scan).
+// Block b of nb = ceil(T / AS_BLK) owns steps [b*AS_BLK, (b+1)*AS_BLK):
+//   1. in-block Hillis-Steele scan (block_scan), the block aggregate is
+//      published with a tagged flag (release);
+//   2. each block waits for the flags of the blocks before it in scan order
+//      (acquire), composes their aggregates with a warp-shuffle scan
+//      (scan_states) and obtains its entry state -- no grid barrier, no
+//      second launch, no counter to reset;
+//   3. the re-walk hands (state before, state after) of every step to the
+//      consumer, whose values are summed per block.
+// Flags carry a per-launch tag, so the workspace needs no initialisation.
+// Blocks only wait on blocks of the same launch and nb <= 128 <= #SMs, so all
+// blocks are co-resident.
+// ---------------------------------------------------------------------------
+#ifdef FCB_SCAN_TL
+// Debug builds only: per-block globaltimer stamps of the one-launch scans.
+__device__ unsigned long long g_scan_tl[AS_BLK][16];
+#define FCB_SCAN_MARK(i)                                                              \
+    do {                                                                              \
+        if (threadIdx.x == 0) {                                                       \
+            unsigned long long t_;                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+            g_scan_tl[blockIdx.x][i] = t_;                                            \
+        }                                                                             \
+    } while (0)
+#else
+#define FCB_SCAN_MARK(i) \
+    do {                 \
+    } while (0)
+#endif
+
+template <int N>
+__device__ __forceinline__ void amap_shfl(AMap<N>& dst, const AMap<N>& src, int delta, bool up) {
+#pragma unroll
+    for (int i = 0; i < N * N; ++i)
+        (&dst.M[0][0])[i] = up ? __shfl_up_sync(0xffffffffu, (&src.M[0][0])[i], delta)
+                               : __shfl_down_sync(0xffffffffu, (&src.M[0][0])[i], delta);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        dst.c[i] = up ? __shfl_up_sync(0xffffffffu, src.c[i], delta)
+                      : __shfl_down_sync(0xffffffffu, src.c[i], delta);
+}
+
+template <int N, int W = AS_BLK / 32>
+struct ScanShared {
+    double tot[W][amap_doubles<N>()];   // scan_states scratch
+    double went[W][N];
+    double btot[W][amap_doubles<N>()];  // in-block warp totals (fused_scan)
+    double bwent[W][N];
+    double red[W];
+};
+
+// Element t is held by thread t of a BLK-thread block.  Returns in `state` the
+// state entering element t: FWD (a_{t-1} o ... o a_0)(init), BWD
+// (a_{t+1} o ... o a_{BLK-1})(init).  `mine` is clobbered.
+template <int N, bool FWD, int BLK>
+__device__ __forceinline__ void scan_states(AMap<N>& mine, const double* init,
+                                            ScanShared<N, BLK / 32>& sh, double* state) {
+    constexpr int W = BLK / 32;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    AMap<N> m, r;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        amap_shfl<N>(m, mine, s, FWD);
+        if (FWD ? lane >= s : lane + s < 32) {
+            amap_compose<N>(mine, m, r);
+            mine = r;
+        }
+    }
+    if (FWD) FCB_SCAN_MARK(10);
+    if (lane == (FWD ? 31 : 0)) amap_copy_to<N>(sh.tot[w], mine);
+    amap_shfl<N>(m, mine, 1, FWD);  // exclusive map inside the warp
+    if (lane == (FWD ? 0 : 31)) amap_identity<N>(m);
+    __syncthreads();
+    if (FWD) FCB_SCAN_MARK(11);
+    if (t == 0) {
+        double s[N], y[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) s[i] = init ? init[i] : 0.0;
+        for (int q = 0; q < W; ++q) {
+            const int ww = FWD ? q : W - 1 - q;
+            AMap<N> a;
+            amap_copy_from<N>(sh.tot[ww], a);
+#pragma unroll
+            for (int i = 0; i < N; ++i) sh.went[ww][i] = s[i];
+            amap_apply<N>(a, s, y);
+#pragma unroll
+            for (int i = 0; i < N; ++i) s[i] = y[i];
+        }
+    }
+    __syncthreads();
+    if (FWD) FCB_SCAN_MARK(12);
+    amap_apply<N>(m, sh.went[w], state);
+}
+
+__device__ __forceinline__ unsigned ld_acquire_flag(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_flag(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Wait (thread t < n) for flags[t] == tag.
+#ifndef FCB_SPIN_SLEEP
+#define FCB_SPIN_SLEEP 32
+#endif
+__device__ __forceinline__ void wait_flag(const unsigned* flags, int t, unsigned tag) {
+    while (ld_acquire_flag(flags + t) != tag) {
+#if FCB_SPIN_SLEEP > 0
+        __nanosleep(FCB_SPIN_SLEEP);
+#endif
+    }
+}
+
+constexpr int FUSED_MAX_BLOCKS = AS_BLK;
+
+inline bool fused_scan_ok(int T) { return T >= 1 && affscan_blocks(T) <= FUSED_MAX_BLOCKS; }
+
+// Workspace of fused scans: per slot nb aggregates and nb flags.
+template <int N>
+inline size_t fused_agg_doubles() {
+    return (size_t)FUSED_MAX_BLOCKS * amap_doubles<N>();
+}
+
+// Optional extra wait folded into the look-back of fused_scan: every block's
+// flag (all nb of them) must carry `tag`; the max of their ints goes to *out.
+struct ExtraWait {
+    const unsigned* flags;
+    const int* vals;
+    int* out;  // shared memory
+    unsigned tag;
+};
+
+// Returns the block's sum of consumer values (every thread).  sbuf: dynamic
+// shared memory of fused_smem_bytes<N>().  Ends with __syncthreads.
+template <int N, bool FWD, class MapFn, class OutFn>
+__device__ double fused_scan(int T, const MapFn& mapf, const OutFn& out, const double* init,
+                             double* agg, unsigned* flags, unsigned tag, double* sbuf,
+                             ScanShared<N>& sh, const ExtraWait* xw = nullptr) {
+    constexpr int AD = amap_doubles<N>();
+    constexpr int W = AS_BLK / 32;
+    const int nb = gridDim.x, b = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int k = b * AS_BLK + t;
+    // 1. in-warp inclusive scan of the step maps (shuffles); the exclusive map
+    //    (neighbour lane's inclusive) is parked in shared memory
+    AMap<N> mine, m, r;
+    if (k < T) mapf(k, mine);
+    else amap_identity<N>(mine);
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        amap_shfl<N>(m, mine, s, FWD);
+        if (FWD ? lane >= s : lane + s < 32) {
+            amap_compose<N>(mine, m, r);
+            mine = r;
+        }
+    }
+    amap_shfl<N>(m, mine, 1, FWD);
+    if (lane == (FWD ? 0 : 31)) amap_identity<N>(m);
+    amap_copy_to<N>(sbuf + t * AD, m);
+    if (lane == (FWD ? 31 : 0)) amap_copy_to<N>(sh.btot[w], mine);
+    __syncthreads();
+    // 2. block aggregate (warp totals composed in scan order), published
+    if (t == 0) {
+        AMap<N> acc, x;
+        amap_copy_from<N>(sh.btot[FWD ? 0 : W - 1], acc);
+#pragma unroll
+        for (int q = 1; q < W; ++q) {
+            amap_copy_from<N>(sh.btot[FWD ? q : W - 1 - q], x);
+            amap_compose<N>(x, acc, r);
+            acc = r;
+        }
+        amap_copy_to<N>(agg + (size_t)b * AD, acc);
+        __threadfence();
+        st_release_flag(flags + b, tag);
+    }
+    FCB_SCAN_MARK(FWD ? 5 : 1);
+    // 3. look-back: predecessors in scan order (FWD [0, b), BWD (b, nb))
+    AMap<N> a;
+    if (FWD ? t < b : (t > b && t < nb)) {
+        wait_flag(flags, t, tag);
+        const double* src = agg + (size_t)t * AD;
+#pragma unroll
+        for (int i = 0; i < N * N; ++i) (&a.M[0][0])[i] = __ldcg(src + i);
+#pragma unroll
+        for (int i = 0; i < N; ++i) a.c[i] = __ldcg(src + N * N + i);
+    } else {
+        amap_identity<N>(a);
+    }
+    if (xw && t < nb) {
+        wait_flag(xw->flags, t, xw->tag);
+        const int f = __ldcg(xw->vals + t);
+        if (f >= 0) atomicMax(xw->out, f);
+    }
+    // reconverge the warp after the divergent spins before any shuffle: a
+    // diverged warp entering the shuffle scan costs ~20 us (measured)
+    __syncwarp();
+    FCB_SCAN_MARK(FWD ? 6 : 2);
+    double st[N];
+    scan_states<N, FWD, AS_BLK>(a, init, sh, st);
+    // 4. block entry -> warp entry states
+    if (t == b) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) sh.bwent[FWD ? 0 : W - 1][i] = st[i];
+    }
+    __syncthreads();
+    if (t == 0) {
+        double x[N], y[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = sh.bwent[FWD ? 0 : W - 1][i];
+#pragma unroll
+        for (int q = 0; q + 1 < W; ++q) {
+            const int ww = FWD ? q : W - 1 - q;
+            AMap<N> tw;
+            amap_copy_from<N>(sh.btot[ww], tw);
+            amap_apply<N>(tw, x, y);
+#pragma unroll
+            for (int i = 0; i < N; ++i) x[i] = sh.bwent[FWD ? ww + 1 : ww - 1][i] = y[i];
+        }
+    }
+    __syncthreads();
+    FCB_SCAN_MARK(FWD ? 7 : 3);
+    // 5. re-walk: after = inclusive map applied to the warp entry, before =
+    //    the exclusive one
+    double before[N], after[N];
+    amap_apply<N>(mine, sh.bwent[w], after);
+    amap_copy_from<N>(sbuf + t * AD, m);
+    amap_apply<N>(m, sh.bwent[w], before);
+    double v = 0.0;
+    if (k < T) v = out(k, before, after);
+    v = warp_sum(v);
+    if (lane == 0) sh.red[w] = v;
+    __syncthreads();
+    double total = 0.0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) total += sh.red[q];
+    __syncthreads();
+    FCB_SCAN_MARK(FWD ? 8 : 4);
+    return total;
+}
+
+template <int N>
+inline size_t fused_smem_bytes() {
+    return (size_t)AS_BLK * amap_doubles<N>() * sizeof(double);
+}
+
+// Per-block values gathered by block 0 in block order (deterministic).
+__device__ __forceinline__ void publish_value(double* vals, unsigned* flags, unsigned tag,
+                                              double v) {
+    if (threadIdx.x == 0) {
+        vals[blockIdx.x] = v;
+        __threadfence();
+        st_release_flag(flags + blockIdx.x, tag);
+    }
+}
+
+// Block 0 only: sum of all blocks' published values, in block order.
+__device__ __forceinline__ double gather_sum(const double* vals, const unsigned* flags,
+                                             unsigned tag, double* s_tmp) {
+    const int nb = gridDim.x, t = threadIdx.x;
+    if (t < nb) {
+        wait_flag(flags, t, tag);
+        s_tmp[t] = __ldcg(vals + t);
+    }
+    __syncthreads();
+    double s = 0.0;
+    for (int q = 0; q < nb; ++q) s += s_tmp[q];
+    return s;
+}
+
+// Host: a fresh tag per fused launch (low 2 bits select the flag use).
+unsigned next_scan_tag();
+
 }  // namespace fcb

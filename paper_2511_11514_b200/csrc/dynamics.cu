@@ -14,6 +14,7 @@
 #include "plan_scan.cuh"
 
 #include <algorithm>
+#include <atomic>
 
 namespace fcb {
 
@@ -249,193 +250,6 @@ __global__ void __launch_bounds__(32) rollout_kernel(const double* __restrict__ 
     }
 }
 
-// Parallel-in-time rollout for linear models.  RK4 with zero-order hold on
-// f = A s + B u is exactly the affine map s' = Phi s + Gam u with
-//   Phi = I + hA + (hA)^2/2 + (hA)^3/6 + (hA)^4/24,
-//   Gam = h (I + hA/2 + (hA)^2/6 + (hA)^3/24) B,
-// so the trajectory is a prefix scan of affine maps (same arithmetic as the
-// RK4 stages, associated differently: results agree to rounding).  Used
-// inside the planner loop; rollout() / the final rollout stay sequential
-// and bit-exact.
-constexpr int RS_THREADS = 256;
-
-template <class Mdl>
-__global__ void __launch_bounds__(RS_THREADS) rollout_scan_kernel(
-    const double* __restrict__ prm, const double* __restrict__ s0, const double* __restrict__ U,
-    int T, double dt, double* __restrict__ S, int d, const double* __restrict__ P,
-    double* __restrict__ X, int* status, int* plan_state, int iteration, double* __restrict__ scratch) {
-    constexpr int N = Mdl::N, M = Mdl::M;
-    constexpr int ASZ = N * N + N;
-    __shared__ double sPhi[N][N], sGam[N][M], sP[3 * N];
-    __shared__ int s_fail;
-    const int tid = threadIdx.x;
-    if (plan_state && *((volatile int*)plan_state) != 0) return;
-    if (tid == 0) {
-        double A[N * N], B[N * M], z0[N] = {}, u0[M] = {};
-        Mdl::jac(z0, u0, prm, A, B);
-        double hA[N][N], Pw[N][N], Phi[N][N], Gs[N][N];
-        for (int i = 0; i < N; ++i)
-            for (int j = 0; j < N; ++j) {
-                hA[i][j] = dt * A[i * N + j];
-                Pw[i][j] = (i == j) ? 1.0 : 0.0;
-                Phi[i][j] = Pw[i][j];
-                Gs[i][j] = Pw[i][j];
-            }
-        const double cphi[5] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0};
-        const double cgam[4] = {1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0};
-        for (int p = 1; p <= 4; ++p) {  // Pw = (hA)^p
-            double Nw[N][N];
-            for (int i = 0; i < N; ++i)
-                for (int j = 0; j < N; ++j) {
-                    double s = 0.0;
-                    for (int q = 0; q < N; ++q) s += Pw[i][q] * hA[q][j];
-                    Nw[i][j] = s;
-                }
-            for (int i = 0; i < N; ++i)
-                for (int j = 0; j < N; ++j) {
-                    Pw[i][j] = Nw[i][j];
-                    Phi[i][j] += cphi[p] * Pw[i][j];
-                    if (p <= 3) Gs[i][j] += cgam[p] * Pw[i][j];
-                }
-        }
-        for (int i = 0; i < N; ++i) {
-            for (int j = 0; j < N; ++j) sPhi[i][j] = Phi[i][j];
-            for (int j = 0; j < M; ++j) {
-                double s = 0.0;
-                for (int q = 0; q < N; ++q) s += Gs[i][q] * B[q * M + j];
-                sGam[i][j] = dt * s;
-            }
-        }
-        for (int i = 0; i < d * N; ++i) sP[i] = P ? P[i] : 0.0;
-        s_fail = 0x7fffffff;
-    }
-    __syncthreads();
-    const int L = (T + RS_THREADS - 1) / RS_THREADS;
-    const int nch = (T + L - 1) / L;
-    const int lo = tid * L, hi = min(lo + L, T);
-    double* affA = scratch;
-    double* affB = scratch + (size_t)RS_THREADS * ASZ;
-    auto input = [&](int k, double (&c)[N]) {
-        double u[M];
-#pragma unroll
-        for (int j = 0; j < M; ++j) u[j] = U[(size_t)k * M + j];
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            double s = 0.0;
-#pragma unroll
-            for (int j = 0; j < M; ++j) s += sGam[i][j] * u[j];
-            c[i] = s;
-        }
-    };
-    if (tid < nch) {  // chunk map: Phi^L and the accumulated input response
-        Aff<N> acc;
-        aff_identity<N>(acc);
-        for (int k = lo; k < hi; ++k) {
-            double c[N], Mn[N][N], cn[N];
-            input(k, c);
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < N; ++q) s += sPhi[i][q] * acc.c[q];
-                cn[i] = s + c[i];
-#pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    double t = 0.0;
-#pragma unroll
-                    for (int q = 0; q < N; ++q) t += sPhi[i][q] * acc.M[q][j];
-                    Mn[i][j] = t;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                acc.c[i] = cn[i];
-#pragma unroll
-                for (int j = 0; j < N; ++j) acc.M[i][j] = Mn[i][j];
-            }
-        }
-        aff_store<N>(affA + (size_t)tid * ASZ, acc);
-    }
-    __syncthreads();
-    double* fs = affA;
-    double* fd = affB;
-    for (int s = 1; s < nch; s <<= 1) {
-        if (tid < nch) {
-            Aff<N> a, b, o;
-            aff_load<N>(fs + (size_t)tid * ASZ, a);
-            if (tid - s >= 0) {
-                aff_load<N>(fs + (size_t)(tid - s) * ASZ, b);
-                aff_compose<N>(a, b, o);
-                aff_store<N>(fd + (size_t)tid * ASZ, o);
-            } else {
-                aff_store<N>(fd + (size_t)tid * ASZ, a);
-            }
-        }
-        __syncthreads();
-        double* t = fs;
-        fs = fd;
-        fd = t;
-    }
-    if (tid < nch) {
-        double st[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) st[i] = s0[i];
-        if (tid > 0) {  // state at chunk start = prefix map applied to s0
-            Aff<N> pre;
-            aff_load<N>(fs + (size_t)(tid - 1) * ASZ, pre);
-            double t2[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < N; ++q) s += pre.M[i][q] * st[q];
-                t2[i] = s + pre.c[i];
-            }
-#pragma unroll
-            for (int i = 0; i < N; ++i) st[i] = t2[i];
-        } else {
-#pragma unroll
-            for (int i = 0; i < N; ++i) S[i] = st[i];
-        }
-        int my_fail = 0x7fffffff;
-        for (int k = lo; k < hi; ++k) {
-            double c[N], sn[N];
-            input(k, c);
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < N; ++q) s += sPhi[i][q] * st[q];
-                sn[i] = s + c[i];
-            }
-#pragma unroll
-            for (int i = 0; i < N; ++i) st[i] = sn[i];
-            if (!all_finite(st, N) && my_fail == 0x7fffffff) my_fail = k + 1;
-#pragma unroll
-            for (int i = 0; i < N; ++i) S[(size_t)(k + 1) * N + i] = st[i];
-            if (X)
-                for (int r = 0; r < d; ++r) {
-                    double a = 0.0;
-#pragma unroll
-                    for (int j = 0; j < N; ++j) a += st[j] * sP[r * N + j];
-                    X[(size_t)k * d + r] = a;
-                }
-        }
-        if (my_fail != 0x7fffffff) atomicMin(&s_fail, my_fail);
-    }
-    __syncthreads();
-    if (tid == 0) {
-        const int f = (s_fail == 0x7fffffff) ? -1 : s_fail;
-        if (status) *status = f;
-        if (plan_state && f >= 0) {
-            plan_state[FCB_STATE_STOP] = 2;
-            plan_state[FCB_STATE_STAGE] = 1;
-            plan_state[FCB_STATE_ITER] = iteration;
-            plan_state[FCB_STATE_INDEX] = f;
-        }
-    }
-}
-
 template <class Mdl>
 __global__ void linearize_kernel(const double* __restrict__ prm, const double* __restrict__ S,
                                  const double* __restrict__ U, int T, double* __restrict__ A,
@@ -577,43 +391,153 @@ static int check_dims(int model, int ns, int m) {
 // Phi = I + hA + (hA)^2/2 + (hA)^3/6 + (hA)^4/24, Gam = h (I + hA/2 + (hA)^2/6
 // + (hA)^3/24) B: one RK4/ZOH step of a linear model as an affine map.
 template <class Mdl>
-__global__ void phigam_kernel(const double* prm, double dt, double* out, const int* gate) {
+__device__ void phigam_compute(const double* prm, double dt, double* out) {
     constexpr int N = Mdl::N, M = Mdl::M;
-    if (threadIdx.x != 0) return;
-    if (gate && *((volatile const int*)gate) != 0) return;
     double A[N * N], B[N * M], z0[N] = {}, u0[M] = {};
     Mdl::jac(z0, u0, prm, A, B);
     double hA[N][N], Pw[N][N], Phi[N][N], Gs[N][N];
+#pragma unroll
     for (int i = 0; i < N; ++i)
+#pragma unroll
         for (int j = 0; j < N; ++j) {
             hA[i][j] = dt * A[i * N + j];
             Pw[i][j] = Phi[i][j] = Gs[i][j] = (i == j) ? 1.0 : 0.0;
         }
     const double cphi[5] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0};
     const double cgam[4] = {1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0};
+#pragma unroll
     for (int p = 1; p <= 4; ++p) {
         double Nw[N][N];
+#pragma unroll
         for (int i = 0; i < N; ++i)
+#pragma unroll
             for (int j = 0; j < N; ++j) {
                 double s = 0.0;
+#pragma unroll
                 for (int q = 0; q < N; ++q) s += Pw[i][q] * hA[q][j];
                 Nw[i][j] = s;
             }
+#pragma unroll
         for (int i = 0; i < N; ++i)
+#pragma unroll
             for (int j = 0; j < N; ++j) {
                 Pw[i][j] = Nw[i][j];
                 Phi[i][j] += cphi[p] * Pw[i][j];
                 if (p <= 3) Gs[i][j] += cgam[p] * Pw[i][j];
             }
     }
+#pragma unroll
     for (int i = 0; i < N; ++i) {
+#pragma unroll
         for (int j = 0; j < N; ++j) out[i * N + j] = Phi[i][j];
+#pragma unroll
         for (int j = 0; j < M; ++j) {
             double s = 0.0;
+#pragma unroll
             for (int q = 0; q < N; ++q) s += Gs[i][q] * B[q * M + j];
             out[N * N + i * M + j] = dt * s;
         }
     }
+}
+
+template <class Mdl>
+__global__ void phigam_kernel(const double* prm, double dt, double* out, const int* gate) {
+    if (threadIdx.x != 0) return;
+    if (gate && *((volatile const int*)gate) != 0) return;
+    phigam_compute<Mdl>(prm, dt, out);
+}
+
+// One-launch rollouts for T <= AS_BLK^2 (fused_scan): Phi/Gam, the scan with
+// the fused state/workspace outputs, and the status epilogue (block 0 takes
+// the first non-finite step over all blocks).
+__device__ __forceinline__ void roll_publish_and_finish(const FusedWs& fw, unsigned* flags,
+                                                        unsigned tag, int first_bad, int* s_min,
+                                                        int* status, int* plan_state,
+                                                        int iteration) {
+    const int t = threadIdx.x, nb = gridDim.x;
+    if (t == 0) {
+        fw.ivals[blockIdx.x] = first_bad;
+        __threadfence();
+        st_release_flag(flags + blockIdx.x, tag);
+    }
+    if (blockIdx.x != 0) return;
+    if (t == 0) *s_min = 0x7f7f7f7f;
+    __syncthreads();
+    if (t < nb) {
+        wait_flag(flags, t, tag);
+        atomicMin(s_min, __ldcg(fw.ivals + t));
+    }
+    __syncthreads();
+    if (t == 0) roll_finish_body(*s_min, status, plan_state, iteration);
+}
+
+template <class Mdl>
+__global__ void __launch_bounds__(AS_BLK)
+    roll_fused_linear_kernel(const double* prm, double dt, const double* s0, const double* U, int T,
+                             double* S, int d, const double* P, double* X, int* status,
+                             int* plan_state, int iteration, FusedWs fw, unsigned tag) {
+    constexpr int N = Mdl::N, M = Mdl::M;
+    extern __shared__ double sbuf[];
+    __shared__ ScanShared<N> sh;
+    __shared__ double pg[N * N + N * M];
+    __shared__ int first_bad, s_min;
+    if (plan_state && *((volatile int*)plan_state) != 0) return;
+    if (threadIdx.x == 0) {
+        phigam_compute<Mdl>(prm, dt, pg);
+        first_bad = 0x7f7f7f7f;
+    }
+    __syncthreads();
+    RollMap<N, M> mapf{pg, U};
+    RollOut<Mdl> out{S, s0, X, P, d, &first_bad, prm, U, dt};
+    fused_scan<N, true>(T, mapf, out, s0, fw.agg0, fw.flags, tag, sbuf, sh);
+    roll_publish_and_finish(fw, fw.flags + AS_BLK, tag, first_bad, &s_min, status, plan_state,
+                            iteration);
+}
+
+template <class Mdl>
+__global__ void __launch_bounds__(AS_BLK)
+    roll_fused_tri_kernel(const double* s0, const double* U, int T, double dt, double* S, int d,
+                          const double* P, double* X, double* dp, int* status, int* plan_state,
+                          int iteration, FusedWs fw, unsigned tag) {
+    extern __shared__ double sbuf[];
+    __shared__ ScanShared<Mdl::NQ> shq;
+    __shared__ ScanShared<Mdl::NP> shp;
+    __shared__ int first_bad, s_min;
+    if (plan_state && *((volatile int*)plan_state) != 0) return;
+    if (threadIdx.x == 0) first_bad = 0x7f7f7f7f;
+    __syncthreads();
+    TriQMap<Mdl> qmap{U, dt};
+    TriQOut<Mdl> qout{U, dt, S, s0, dp, &first_bad};
+    fused_scan<Mdl::NQ, true>(T, qmap, qout, s0 + Mdl::QOFF, fw.agg0, fw.flags, tag, sbuf, shq);
+    TriPMap<Mdl> pmap{dp};
+    TriPOut<Mdl> pout{S, X, P, d, &first_bad};
+    fused_scan<Mdl::NP, true>(T, pmap, pout, s0, fw.agg1, fw.flags + AS_BLK, tag, sbuf, shp);
+    roll_publish_and_finish(fw, fw.flags + 2 * AS_BLK, tag, first_bad, &s_min, status, plan_state,
+                            iteration);
+}
+
+static std::atomic<unsigned> g_scan_tag{0x5eed0000u};
+unsigned next_scan_tag() { return g_scan_tag.fetch_add(1u, std::memory_order_relaxed); }
+
+static FusedWs fused_take(Arena& ar) {
+    FusedWs f{};
+    f.agg0 = ar.take<double>(fused_agg_doubles<6>());
+    f.agg1 = ar.take<double>(fused_agg_doubles<6>());
+    f.vals = ar.take<double>(FUSED_MAX_BLOCKS);
+    f.ivals = ar.take<int>(FUSED_MAX_BLOCKS);
+    f.flags = ar.take<unsigned>(4 * AS_BLK);
+    return f;
+}
+
+// dynamic shared memory of a fused kernel (the in-block scan buffers)
+template <class Kern>
+static size_t fused_smem(Kern k, size_t bytes) {
+    static size_t set = 0;  // per kernel instantiation
+    if (bytes > set) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        set = bytes;
+    }
+    return bytes;
 }
 
 struct RollWs {
@@ -621,6 +545,7 @@ struct RollWs {
     double* scan;
     double* dp;
     int* first_bad;
+    FusedWs fw;
     size_t bytes;
 };
 
@@ -631,6 +556,7 @@ static RollWs roll_layout(int ns, int T, void* ws) {
     L.scan = ar.take<double>(affscan_scratch_doubles<6>(T));  // sized for the largest N
     L.dp = ar.take<double>((size_t)T * 3);                    // triangular models' increments
     L.first_bad = ar.take<int>(4);
+    L.fw = fused_take(ar);
     L.bytes = ar.off + 256;
     (void)ns;
     return L;
@@ -643,6 +569,17 @@ static int launch_rollout(int method, const double* prm, const double* s0, const
                           double dt, double* S, int d, const double* P, double* X, int* status,
                           int* plan_state, int iteration, double* ws, cudaStream_t st) {
     constexpr int N = Mdl::N, M = Mdl::M;
+    if constexpr (Mdl::LINEAR) {
+        if (method == 1 && ws != nullptr && fused_scan_ok(T)) {
+            RollWs L = roll_layout(N, T, ws);
+            auto kern = roll_fused_linear_kernel<Mdl>;
+            const size_t smem = fused_smem(kern, fused_smem_bytes<N>());
+            kern<<<affscan_blocks(T), AS_BLK, smem, st>>>(prm, dt, s0, U, T, S, d, P, X, status,
+                                                          plan_state, iteration, L.fw,
+                                                          next_scan_tag());
+            return 1;
+        }
+    }
     if (Mdl::LINEAR && method == 1 && ws != nullptr) {
         RollWs L = roll_layout(N, T, ws);
         cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st);
@@ -655,6 +592,16 @@ static int launch_rollout(int method, const double* prm, const double* s0, const
         return n + 2;
     }
     if constexpr (Mdl::TRIANGULAR) {
+        if (method == 1 && ws != nullptr && fused_scan_ok(T)) {
+            RollWs L = roll_layout(N, T, ws);
+            auto kern = roll_fused_tri_kernel<Mdl>;
+            constexpr int NMAX = Mdl::NQ > Mdl::NP ? Mdl::NQ : Mdl::NP;
+            const size_t smem = fused_smem(kern, fused_smem_bytes<NMAX>());
+            kern<<<affscan_blocks(T), AS_BLK, smem, st>>>(s0, U, T, dt, S, d, P, X, L.dp, status,
+                                                          plan_state, iteration, L.fw,
+                                                          next_scan_tag());
+            return 1;
+        }
         if (method == 1 && ws != nullptr) {
             RollWs L = roll_layout(N, T, ws);
             cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st);
@@ -701,11 +648,12 @@ int linearize(int model, int ns, int m, const double* prm, const double* S, cons
 }
 
 // Workspace of the two-phase LQR: Riccati scan aggregates, per-step Riccati
-// outputs (K, H^-1 G', Phi, Acl, G), d, the affine-scan scratch and a status
-// word.
+// outputs (K, H^-1 G', Acl, G; element-major), d, the affine-scan scratch, a
+// status word and the one-launch scan flags.
 struct LqrWs {
-    double *agg, *K, *Lg, *Phi, *Acl, *Gm, *dff, *scan;
+    double *agg, *K, *Lg, *Acl, *Gm, *dff, *scan;
     int* fail;
+    FusedWs fw;
     size_t bytes;
 };
 
@@ -715,12 +663,12 @@ static LqrWs lqr_layout(int ns, int m, int T, void* ws) {
     L.agg = ar.take<double>(2 * (size_t)LQR_THREADS * 3 * ns * ns);
     L.K = ar.take<double>((size_t)T * m * ns);
     L.Lg = ar.take<double>((size_t)T * m * ns);
-    L.Phi = ar.take<double>((size_t)T * ns * ns);
     L.Acl = ar.take<double>((size_t)T * ns * ns);
     L.Gm = ar.take<double>((size_t)T * ns * m);
     L.dff = ar.take<double>((size_t)T * m);
     L.scan = ar.take<double>(affscan_scratch_doubles<6>(T));
     L.fail = ar.take<int>(4);
+    L.fw = fused_take(ar);
     L.bytes = ar.off + 256;
     return L;
 }
@@ -736,7 +684,6 @@ static RicArgs ric_args(const LqrWs& L, int T, double dt, const double* Q, const
     r.agg = L.agg;
     r.K = L.K;
     r.Lg = L.Lg;
-    r.Phi = L.Phi;
     r.Acl = L.Acl;
     r.Gm = L.Gm;
     r.fail = L.fail;
@@ -750,17 +697,37 @@ static int affine_phase(const LqrWs& L, const double* K, double* dff, int T, dou
                         const double* Q, const double* R, const Flow& flow, double* v, double* z,
                         const double* U, double* U_next, double eta, const double* clamp,
                         double* cost, double* lqr_costs, int* plan_state, int iteration,
-                        cudaStream_t st) {
+                        int reset_fail, cudaStream_t st) {
+    EtaMap<N, Flow> emap{L.Acl, Q, dt, T, flow};
+    EtaOut<N, M> eout{L.Lg, dff, L.fail, T};
+    ZMap<N, M> zmap{L.Acl, L.Gm, dff, T};
+    ZOut<N, M, Flow> zout{K, T, dff, Q, R, dt, flow, L.fail, v, z, U, U_next, eta, clamp};
+    if (fused_scan_ok(T)) {
+        auto kern = affine_fused_kernel<N, M, Flow>;
+        const size_t smem = fused_smem(kern, fused_smem_bytes<N>());
+        kern<<<affscan_blocks(T), AS_BLK, smem, st>>>(T, emap, eout, zmap, zout, L.fw,
+                                                      next_scan_tag(), L.fail, reset_fail, cost,
+                                                      lqr_costs, plan_state, iteration);
+        return 1;
+    }
+    if (reset_fail) cudaMemsetAsync(L.fail, 0xff, sizeof(int), st);
     const AffScanBufs b = affscan_bufs<N>(L.scan, T);
-    EtaMap<N, Flow> emap{L.Phi, Q, dt, flow};
-    EtaOut<N, M> eout{L.Lg, dff, L.fail};
     int n = affscan_run<N, false>(T, emap, eout, nullptr, b, plan_state, st);
-    ZMap<N, M> zmap{L.Acl, L.Gm, dff};
-    ZOut<N, M, Flow> zout{K, dff, Q, R, dt, flow, L.fail, v, z, U, U_next, eta, clamp};
     n += affscan_run<N, true>(T, zmap, zout, nullptr, b, plan_state, st);
     lqr_finish_kernel<<<1, 32, 0, st>>>(affscan_blocks(T), b.red, L.fail, cost, lqr_costs,
                                         plan_state, iteration, plan_state != nullptr);
     return n + 1;
+}
+
+// X[e * T + k] -> Y[k * E + e]
+__global__ void step_major_kernel(const double* __restrict__ X, int T, int E,
+                                  double* __restrict__ Y) {
+    const size_t n = (size_t)T * E;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const size_t k = i / E, e = i % E;
+        Y[i] = X[e * T + k];
+    }
 }
 
 template <int N, int M>
@@ -768,11 +735,16 @@ static int lqr_solve_t(int T, double dt, const double* A, const double* B, const
                        const double* R, const double* a, double* v, double* z, double* K,
                        double* dff, double* scal, const LqrWs& L, cudaStream_t st) {
     RicArgs r = ric_args(L, T, dt, Q, R);
-    if (K) r.K = K;
     lqr_riccati_arrays_kernel<N, M><<<1, LQR_THREADS, 0, st>>>(r, A, B);
     ArrayFlow<N> fl{a};
-    return 1 + affine_phase<N, M>(L, r.K, dff ? dff : L.dff, T, dt, Q, R, fl, v, z, nullptr,
-                                  nullptr, 0.0, nullptr, scal, nullptr, nullptr, 0, st);
+    int n = 1 + affine_phase<N, M>(L, L.K, dff ? dff : L.dff, T, dt, Q, R, fl, v, z, nullptr,
+                                   nullptr, 0.0, nullptr, scal, nullptr, nullptr, 0, 0, st);
+    if (K) {  // gains to the caller's step-major layout [T][M][N]
+        const int blocks = std::min(4 * sm_count(), (T * M * N + 255) / 256);
+        step_major_kernel<<<blocks, 256, 0, st>>>(L.K, T, M * N, K);
+        ++n;
+    }
+    return n;
 }
 
 int lqr_solve(int ns, int m, int T, double dt, const double* A, const double* B, const double* Q,
@@ -818,12 +790,11 @@ static int launch_plan_update(int mode, const LqrWs& L, int T, double dt, const 
         r.iteration = iteration;
         plan_riccati_kernel<Mdl><<<1, LQR_THREADS, 0, st>>>(r, prm, S, U);
         n = 1;
-    } else {
-        cudaMemsetAsync(L.fail, 0xff, sizeof(int), st);  // -1: the stored Riccati phase is valid
     }
+    // mode 1: fail := -1, the stored Riccati phase is valid
     LiftedFlow<N> fl{flow, P, d};
     return n + affine_phase<N, M>(L, L.K, L.dff, T, dt, Q, R, fl, nullptr, nullptr, U, Unext, eta,
-                                  clamp, nullptr, lqr_costs, plan_state, iteration, st);
+                                  clamp, nullptr, lqr_costs, plan_state, iteration, mode == 1, st);
 }
 
 int plan_update(int model, int ns, int m, const double* prm, const double* S, const double* U,
@@ -846,3 +817,15 @@ int plan_update(int model, int ns, int m, const double* prm, const double* S, co
 }
 
 }  // namespace fcb
+
+// Debug: per-block stamps of the last one-launch scan (FCB_SCAN_TL builds).
+extern "C" FCB_API int fcb_debug_scan_timeline(unsigned long long* host_out) {
+#ifdef FCB_SCAN_TL
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(host_out, fcb::g_scan_tl, sizeof(fcb::g_scan_tl));
+    return fcb::AS_BLK * 16;
+#else
+    (void)host_out;
+    return 0;
+#endif
+}

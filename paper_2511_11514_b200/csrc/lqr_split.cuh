@@ -173,11 +173,11 @@ struct RicArgs {
     const double* Q;
     const double* R;
     double* agg;  // 2 * LQR_THREADS * 3N^2
-    double* K;    // T*M*N
-    double* Lg;   // T*M*N   H^-1 G'
-    double* Phi;  // T*N*N
-    double* Acl;  // T*N*N
-    double* Gm;   // T*N*M
+    // per-step outputs, element-major: X[e * T + k]
+    double* K;    // M*N x T
+    double* Lg;   // M*N x T   H^-1 G'
+    double* Acl;  // N*N x T   closed loop F - G K
+    double* Gm;   // N*M x T
     int* fail;
     int* plan_state;
     int iteration;
@@ -357,17 +357,16 @@ __device__ void riccati_body(const Jac& jac, const RicArgs& p) {
                     for (int c2 = r + 1; c2 < M; ++c2) v -= H[r][c2] * rhs[c2][q];
                     rhs[r][q] = v / H[r][r];
                 }
-            double* Kk = p.K + (size_t)k * M * N;
-            double* Lk = p.Lg + (size_t)k * M * N;
+            // per-step outputs, element-major ([element][T]): the affine scans
+            // read one element of consecutive steps per warp load
+            const size_t TT = (size_t)p.T;
 #pragma unroll
             for (int i = 0; i < M; ++i)
 #pragma unroll
                 for (int j = 0; j < N; ++j) {
-                    Kk[i * N + j] = rhs[i][j];
-                    Lk[i * N + j] = rhs[i][N + j];
+                    p.K[(i * N + j) * TT + k] = rhs[i][j];
+                    p.Lg[(i * N + j) * TT + k] = rhs[i][N + j];
                 }
-            double* Ak = p.Acl + (size_t)k * N * N;
-            double* Gk = p.Gm + (size_t)k * N * M;
 #pragma unroll
             for (int i = 0; i < N; ++i) {
 #pragma unroll
@@ -375,10 +374,10 @@ __device__ void riccati_body(const Jac& jac, const RicArgs& p) {
                     double s = 0.0;
 #pragma unroll
                     for (int q = 0; q < M; ++q) s += G[i][q] * rhs[q][j];
-                    Ak[i * N + j] = F[i][j] - s;
+                    p.Acl[(i * N + j) * TT + k] = F[i][j] - s;
                 }
 #pragma unroll
-                for (int j = 0; j < M; ++j) Gk[i * M + j] = G[i][j];
+                for (int j = 0; j < M; ++j) p.Gm[(i * M + j) * TT + k] = G[i][j];
             }
             // Phi = (I + C_k J2)^-1 F ; J_k = Phi' J2 F + 2 Qb
             ElemR<N> e;
@@ -389,9 +388,6 @@ __device__ void riccati_body(const Jac& jac, const RicArgs& p) {
 #pragma unroll
                 for (int j = 0; j < N; ++j) X[i][j] = F[i][j];
             solve_ipcj<N, N>(e.C, J2, X);
-            double* Pk = p.Phi + (size_t)k * N * N;
-#pragma unroll
-            for (int i = 0; i < N * N; ++i) Pk[i] = (&X[0][0])[i];
             double JF[N][N], Jn[N][N];
 #pragma unroll
             for (int i = 0; i < N; ++i)
@@ -431,274 +427,6 @@ __device__ void riccati_body(const Jac& jac, const RicArgs& p) {
             p.plan_state[FCB_STATE_STAGE] = 3;
             p.plan_state[FCB_STATE_ITER] = p.iteration;
             p.plan_state[FCB_STATE_INDEX] = sh.fail;
-        }
-    }
-}
-
-struct AffArgs {
-    int T;
-    double dt;
-    const double* Q;
-    const double* R;
-    const double* K;
-    const double* Lg;
-    const double* Phi;
-    const double* Acl;
-    const double* Gm;
-    double* aff;  // 2 * LQR_THREADS * (N*N + N)
-    double* dff;  // T*M
-    double* v;    // nullable T*M
-    double* z;    // nullable (T+1)*N
-    double* cost; // nullable
-    int* fail;    // Riccati status in, overall status out
-    const double* U;
-    double* U_next;
-    double eta;
-    const double* clamp;
-    double* lqr_costs;
-    int* plan_state;
-    int iteration;
-};
-
-// Affine phase: eta (backward affine scan), d, then z/v/cost/U (forward).
-template <int N, int M, class Flow>
-__device__ void affine_body(const Flow& flow, const AffArgs& p) {
-    constexpr int ASZ = N * N + N;
-    __shared__ LqrShared<N, M> sh;
-    lqr_shared_init<N, M>(sh, p.Q, p.R, p.dt);
-    if (*((volatile const int*)p.fail) >= 0) return;  // Riccati phase failed
-    const int tid = threadIdx.x;
-    const int T = p.T;
-    const int L = (T + LQR_THREADS - 1) / LQR_THREADS;
-    const int nch = (T + L - 1) / L;
-    const int lo = tid * L, hi = min(lo + L, T);
-    double* src = p.aff;
-    double* dst = p.aff + (size_t)LQR_THREADS * ASZ;
-
-    // m_k: v -> Phi_k' v + h_k,  h_k = 2 Qb a_k
-    auto map_k = [&](int k, Aff<N>& m) {
-        double ak[N];
-        flow.get(k, ak);
-        const double* Pk = p.Phi + (size_t)k * N * N;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            double s = 0.0;
-#pragma unroll
-            for (int q = 0; q < N; ++q) s += sh.Qb[i][q] * ak[q];
-            m.c[i] = 2.0 * s;
-#pragma unroll
-            for (int j = 0; j < N; ++j) m.M[i][j] = __ldcg(Pk + j * N + i);  // transpose
-        }
-    };
-    if (tid < nch) {  // B1: chunk maps m_lo o ... o m_{hi-1}
-        Aff<N> acc, m, tmp;
-        aff_identity<N>(acc);
-        for (int k = hi - 1; k >= lo; --k) {
-            map_k(k, m);
-            aff_compose<N>(m, acc, tmp);
-            acc = tmp;
-        }
-        aff_store<N>(src + (size_t)tid * ASZ, acc);
-    }
-    __syncthreads();
-    for (int s = 1; s < nch; s <<= 1) {  // B2: inclusive suffix scan
-        if (tid < nch) {
-            Aff<N> a, b, o;
-            aff_load<N>(src + (size_t)tid * ASZ, a);
-            if (tid + s < nch) {
-                aff_load<N>(src + (size_t)(tid + s) * ASZ, b);
-                aff_compose<N>(a, b, o);
-                aff_store<N>(dst + (size_t)tid * ASZ, o);
-            } else {
-                aff_store<N>(dst + (size_t)tid * ASZ, a);
-            }
-        }
-        __syncthreads();
-        double* t = src;
-        src = dst;
-        dst = t;
-    }
-    if (tid < nch) {  // B3: re-walk: d_k = 1/2 Lg_k eta_{k+1}
-        double v[N];
-        if (tid + 1 < nch) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) v[i] = __ldcg(src + (size_t)(tid + 1) * ASZ + N * N + i);
-        } else {
-#pragma unroll
-            for (int i = 0; i < N; ++i) v[i] = 0.0;
-        }
-        int local_fail = -1;
-        for (int k = hi - 1; k >= lo; --k) {
-            const double* Lk = p.Lg + (size_t)k * M * N;
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) s += __ldcg(Lk + i * N + j) * v[j];
-                p.dff[(size_t)k * M + i] = 0.5 * s;
-            }
-            Aff<N> m;
-            map_k(k, m);
-            double vn[N];
-            bool finite = true;
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) s += m.M[i][j] * v[j];
-                vn[i] = s + m.c[i];
-                finite = finite && isfinite(vn[i]);
-            }
-#pragma unroll
-            for (int i = 0; i < N; ++i) v[i] = vn[i];
-            if (!finite && local_fail < 0) local_fail = k;
-        }
-        if (local_fail >= 0) atomicMax(&sh.fail, local_fail);
-    }
-    __syncthreads();
-    if (sh.fail >= 0) {
-        if (tid == 0) {
-            *p.fail = sh.fail;
-            if (p.plan_state) {
-                p.plan_state[FCB_STATE_STOP] = 2;
-                p.plan_state[FCB_STATE_STAGE] = 3;
-                p.plan_state[FCB_STATE_ITER] = p.iteration;
-                p.plan_state[FCB_STATE_INDEX] = sh.fail;
-            }
-        }
-        return;
-    }
-    // forward: z_{k+1} = Acl_k z_k + G_k d_k
-    auto fmap = [&](int k, Aff<N>& a) {
-        const double* Ak = p.Acl + (size_t)k * N * N;
-        const double* Gk = p.Gm + (size_t)k * N * M;
-        double dk[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) dk[i] = __ldcg(p.dff + (size_t)k * M + i);
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            double cc = 0.0;
-#pragma unroll
-            for (int q = 0; q < M; ++q) cc += __ldcg(Gk + i * M + q) * dk[q];
-            a.c[i] = cc;
-#pragma unroll
-            for (int j = 0; j < N; ++j) a.M[i][j] = __ldcg(Ak + i * N + j);
-        }
-    };
-    __syncthreads();
-    src = p.aff;
-    dst = p.aff + (size_t)LQR_THREADS * ASZ;
-    if (tid < nch) {  // F1: chunk compositions
-        Aff<N> acc, m, tmp;
-        aff_identity<N>(acc);
-        for (int k = lo; k < hi; ++k) {
-            fmap(k, m);
-            aff_compose<N>(m, acc, tmp);
-            acc = tmp;
-        }
-        aff_store<N>(src + (size_t)tid * ASZ, acc);
-    }
-    __syncthreads();
-    for (int s = 1; s < nch; s <<= 1) {  // F2: inclusive prefix scan
-        if (tid < nch) {
-            Aff<N> a, b, o;
-            aff_load<N>(src + (size_t)tid * ASZ, a);
-            if (tid - s >= 0) {
-                aff_load<N>(src + (size_t)(tid - s) * ASZ, b);
-                aff_compose<N>(a, b, o);
-                aff_store<N>(dst + (size_t)tid * ASZ, o);
-            } else {
-                aff_store<N>(dst + (size_t)tid * ASZ, a);
-            }
-        }
-        __syncthreads();
-        double* t = src;
-        src = dst;
-        dst = t;
-    }
-    double cost_part = 0.0;
-    if (tid < nch) {  // F3: re-walk: z, v*, cost, control update
-        double zz[N];
-        if (tid == 0) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) zz[i] = 0.0;
-            if (p.z)
-#pragma unroll
-                for (int i = 0; i < N; ++i) p.z[i] = 0.0;
-        } else {
-#pragma unroll
-            for (int i = 0; i < N; ++i) zz[i] = __ldcg(src + (size_t)(tid - 1) * ASZ + N * N + i);
-        }
-        for (int k = lo; k < hi; ++k) {
-            double ak[N];
-            flow.get(k, ak);
-            const double* Kk = p.K + (size_t)k * M * N;
-            double vk[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) s += __ldcg(Kk + i * N + j) * zz[j];
-                vk[i] = __ldcg(p.dff + (size_t)k * M + i) - s;
-            }
-            double e[N], c1 = 0.0, c2 = 0.0;
-#pragma unroll
-            for (int i = 0; i < N; ++i) e[i] = ak[i] - zz[i];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) s += sh.Qb[i][j] * e[j];
-                c1 += e[i] * s;
-            }
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < M; ++j) s += sh.Rb[i][j] * vk[j];
-                c2 += vk[i] * s;
-            }
-            cost_part += c1 + c2;
-            if (p.v)
-#pragma unroll
-                for (int i = 0; i < M; ++i) p.v[(size_t)k * M + i] = vk[i];
-            if (p.U_next) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    double u = p.U[(size_t)k * M + i] + p.eta * vk[i];
-                    if (p.clamp) {
-                        const double b = p.clamp[i];
-                        u = fmin(fmax(u, -b), b);
-                    }
-                    p.U_next[(size_t)k * M + i] = u;
-                }
-            }
-            const double* Ak = p.Acl + (size_t)k * N * N;
-            const double* Gk = p.Gm + (size_t)k * N * M;
-            double zn[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) s += __ldcg(Ak + i * N + j) * zz[j];
-#pragma unroll
-                for (int j = 0; j < M; ++j) s += __ldcg(Gk + i * M + j) * __ldcg(p.dff + (size_t)k * M + j);
-                zn[i] = s;
-            }
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                zz[i] = zn[i];
-                if (p.z) p.z[(size_t)(k + 1) * N + i] = zz[i];
-            }
-        }
-    }
-    const double total = block_sum<LQR_THREADS>(cost_part, sh.red);
-    if (tid == 0) {
-        *p.fail = -1;
-        if (p.cost) *p.cost = total;
-        if (p.plan_state) {
-            p.lqr_costs[p.iteration] = total;
-            p.plan_state[FCB_STATE_UPDATES] = p.iteration + 1;
         }
     }
 }

@@ -12,17 +12,21 @@ namespace fcb {
 // ---------------------------------------------------------------------------
 // LQR affine phase
 // ---------------------------------------------------------------------------
-// backward: eta_k = Phi_k' eta_{k+1} + 2 Qb a_k
+// The Riccati outputs are element-major (X[e * T + k], lqr_split.cuh), so a
+// warp reading one element of 32 consecutive steps is one coalesced load.
+//
+// backward: eta_k = Acl_k' eta_{k+1} + 2 Qb a_k  (eta = -2 p of lqr.py:190,
+// with the reference's closed = F - G K)
 template <int N, class Flow>
 struct EtaMap {
-    const double* Phi;
+    const double* Acl;
     const double* Q;
     double dt;
+    int T;
     Flow flow;
     __device__ void operator()(int k, AMap<N>& m) const {
         double ak[N];
         flow.get(k, ak);
-        const double* Pk = Phi + (size_t)k * N * N;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
             double s = 0.0;
@@ -30,7 +34,7 @@ struct EtaMap {
             for (int q = 0; q < N; ++q) s += Q[i * N + q] * ak[q];
             m.c[i] = 2.0 * dt * s;
 #pragma unroll
-            for (int j = 0; j < N; ++j) m.M[i][j] = Pk[j * N + i];
+            for (int j = 0; j < N; ++j) m.M[i][j] = Acl[(size_t)(j * N + i) * T + k];
         }
     }
 };
@@ -41,13 +45,13 @@ struct EtaOut {
     const double* Lg;
     double* dff;
     int* fail;
+    int T;
     __device__ double operator()(int k, const double* e_next, const double* e_k) const {
-        const double* Lk = Lg + (size_t)k * M * N;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < N; ++j) s += Lk[i * N + j] * e_next[j];
+            for (int j = 0; j < N; ++j) s += Lg[(size_t)(i * N + j) * T + k] * e_next[j];
             dff[(size_t)k * M + i] = 0.5 * s;
         }
         bool finite = true;
@@ -64,9 +68,8 @@ struct ZMap {
     const double* Acl;
     const double* Gm;
     const double* dff;
+    int T;
     __device__ void operator()(int k, AMap<N>& m) const {
-        const double* Ak = Acl + (size_t)k * N * N;
-        const double* Gk = Gm + (size_t)k * N * M;
         double dk[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) dk[i] = dff[(size_t)k * M + i];
@@ -74,10 +77,10 @@ struct ZMap {
         for (int i = 0; i < N; ++i) {
             double cc = 0.0;
 #pragma unroll
-            for (int q = 0; q < M; ++q) cc += Gk[i * M + q] * dk[q];
+            for (int q = 0; q < M; ++q) cc += Gm[(size_t)(i * M + q) * T + k] * dk[q];
             m.c[i] = cc;
 #pragma unroll
-            for (int j = 0; j < N; ++j) m.M[i][j] = Ak[i * N + j];
+            for (int j = 0; j < N; ++j) m.M[i][j] = Acl[(size_t)(i * N + j) * T + k];
         }
     }
 };
@@ -85,7 +88,8 @@ struct ZMap {
 // consumer: v_k = d_k - K_k z_k, the stage cost, z, the control update
 template <int N, int M, class Flow>
 struct ZOut {
-    const double* K;
+    const double* K;  // element-major
+    int T;
     const double* dff;
     const double* Q;
     const double* R;
@@ -100,13 +104,12 @@ struct ZOut {
     const double* clamp;
     __device__ double operator()(int k, const double* zk, const double* zk1) const {
         if (*((volatile const int*)fail) >= 0) return 0.0;
-        const double* Kk = K + (size_t)k * M * N;
         double vk[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < N; ++j) s += Kk[i * N + j] * zk[j];
+            for (int j = 0; j < N; ++j) s += K[(size_t)(i * N + j) * T + k] * zk[j];
             vk[i] = dff[(size_t)k * M + i] - s;
         }
         double ak[N], e[N];
@@ -149,12 +152,10 @@ struct ZOut {
     }
 };
 
-// After both scans: total cost (fixed order), status, planner hooks.
-__global__ void lqr_finish_kernel(int nb, const double* red, int* fail, double* cost,
-                                  double* lqr_costs, int* plan_state, int iteration, int gated) {
-    if (threadIdx.x != 0) return;
-    if (gated && plan_state && *((volatile int*)plan_state) != 0) return;
-    const int f = *fail;
+// After both scans: total cost, status, planner hooks.
+__device__ __forceinline__ void lqr_finish_body(double total, int* fail, double* cost,
+                                                double* lqr_costs, int* plan_state, int iteration) {
+    const int f = *((volatile int*)fail);
     if (f >= 0) {
         if (plan_state) {
             plan_state[FCB_STATE_STOP] = 2;
@@ -164,13 +165,74 @@ __global__ void lqr_finish_kernel(int nb, const double* red, int* fail, double* 
         }
         return;
     }
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += red[b];
-    if (cost) *cost = s;
+    if (cost) *cost = total;
     if (plan_state) {
-        lqr_costs[iteration] = s;
+        lqr_costs[iteration] = total;
         plan_state[FCB_STATE_UPDATES] = iteration + 1;
     }
+}
+
+__global__ void lqr_finish_kernel(int nb, const double* red, int* fail, double* cost,
+                                  double* lqr_costs, int* plan_state, int iteration, int gated) {
+    if (threadIdx.x != 0) return;
+    if (gated && plan_state && *((volatile int*)plan_state) != 0) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += red[b];
+    lqr_finish_body(s, fail, cost, lqr_costs, plan_state, iteration);
+}
+
+// Flag slots of the one-launch kernels (per launch tag, AS_BLK flags each).
+struct FusedWs {
+    double* agg0;      // FUSED_MAX_BLOCKS maps (N <= 6)
+    double* agg1;
+    double* vals;      // FUSED_MAX_BLOCKS
+    int* ivals;        // FUSED_MAX_BLOCKS
+    unsigned* flags;   // 4 * AS_BLK
+};
+
+// The whole affine phase in one launch for T <= AS_BLK^2: eta scan (emits d),
+// the blocks' eta status, z scan (v, cost, z, U update) and the finish.
+template <int N, int M, class Flow>
+__global__ void __launch_bounds__(AS_BLK)
+    affine_fused_kernel(int T, EtaMap<N, Flow> emap, EtaOut<N, M> eout, ZMap<N, M> zmap,
+                        ZOut<N, M, Flow> zout, FusedWs fw, unsigned tag, int* fail, int reset_fail,
+                        double* cost, double* lqr_costs, int* plan_state, int iteration) {
+    extern __shared__ double sbuf[];
+    __shared__ ScanShared<N> sh;
+    __shared__ int s_fail_eta, s_fail_all;
+    __shared__ double s_tmp[AS_BLK];
+    if (plan_state && *((volatile int*)plan_state) != 0) return;
+    FCB_SCAN_MARK(0);
+    const int t = threadIdx.x;
+    if (t == 0) {
+        s_fail_eta = -1;
+        s_fail_all = reset_fail ? -1 : *((volatile int*)fail);
+    }
+    __syncthreads();
+    EtaOut<N, M> eo = eout;
+    eo.fail = &s_fail_eta;
+    fused_scan<N, false>(T, emap, eo, nullptr, fw.agg0, fw.flags, tag, sbuf, sh);
+    if (t == 0) {
+        fw.ivals[blockIdx.x] = s_fail_eta;
+        __threadfence();
+        st_release_flag(fw.flags + AS_BLK + blockIdx.x, tag);
+    }
+    // the z consumer skips every step once any eta is non-finite: every
+    // block's eta status is gathered during the z look-back
+    ZOut<N, M, Flow> zo = zout;
+    zo.fail = &s_fail_all;
+    const ExtraWait xw{fw.flags + AS_BLK, fw.ivals, &s_fail_all, tag};
+    const double part = fused_scan<N, true>(T, zmap, zo, nullptr, fw.agg1, fw.flags + 2 * AS_BLK,
+                                            tag, sbuf, sh, &xw);
+    publish_value(fw.vals, fw.flags + 3 * AS_BLK, tag, part);
+    if (blockIdx.x == 0) {
+        const double total = gather_sum(fw.vals, fw.flags + 3 * AS_BLK, tag, s_tmp);
+        if (t == 0) {
+            *fail = s_fail_all;
+            lqr_finish_body(total, fail, cost, lqr_costs, plan_state, iteration);
+        }
+    }
+    FCB_SCAN_MARK(9);
 }
 
 // ---------------------------------------------------------------------------
@@ -384,11 +446,10 @@ struct TriPOut {
     }
 };
 
-__global__ void roll_finish_kernel(int* first_bad, int* status, int* plan_state, int iteration) {
-    if (threadIdx.x != 0) return;
-    if (plan_state && *((volatile int*)plan_state) != 0) return;
-    // first_bad starts at 0x7f7f7f7f (byte memset): no non-finite state seen
-    const int f = (*first_bad >= 0x7f7f7f7f) ? -1 : *first_bad;
+// first_bad starts at 0x7f7f7f7f (byte memset): no non-finite state seen
+__device__ __forceinline__ void roll_finish_body(int first_bad, int* status, int* plan_state,
+                                                 int iteration) {
+    const int f = (first_bad >= 0x7f7f7f7f) ? -1 : first_bad;
     if (status) *status = f;
     if (plan_state && f >= 0) {
         plan_state[FCB_STATE_STOP] = 2;
@@ -396,6 +457,12 @@ __global__ void roll_finish_kernel(int* first_bad, int* status, int* plan_state,
         plan_state[FCB_STATE_ITER] = iteration;
         plan_state[FCB_STATE_INDEX] = f;
     }
+}
+
+__global__ void roll_finish_kernel(int* first_bad, int* status, int* plan_state, int iteration) {
+    if (threadIdx.x != 0) return;
+    if (plan_state && *((volatile int*)plan_state) != 0) return;
+    roll_finish_body(*first_bad, status, plan_state, iteration);
 }
 
 }  // namespace fcb

@@ -30,6 +30,10 @@ def phases(iters=20):
     pt = run.result.phase_times
     print(f"iters={iters} total={pt.total*1e3:.1f}ms flow={pt.flow*1e3:.1f}ms "
           f"lqr={pt.lqr*1e3:.1f}ms rollout={pt.rollout*1e3:.1f}ms pairs={run.pairs:.3e}")
+    lg = run.flow_log
+    if lg is not None and len(lg):
+        print(f"sinkhorn iterations per flow: cross mean {lg[:, 1].mean():.1f} max {lg[:, 1].max():.0f}"
+              f" | self mean {lg[:, 2].mean():.1f} max {lg[:, 2].max():.0f}")
 
 
 def solve(reps=5, n=2000, m=10_000, iters=10):

@@ -81,6 +81,24 @@ def test_lqr_golden(T):
     assert sol.cost == pytest.approx(float(g[p + "cost"]), rel=1e-10)
 
 
+@pytest.mark.parametrize("T,n,m", [(4096, 4, 2), (4097, 4, 2), (2049, 6, 3), (12000, 3, 2)])
+def test_lqr_long_horizon_matches_oracle(T, n, m):
+    """Both affine-phase paths: the single-CTA fused scan (T <= 8 * block) and
+    the three-kernel multi-CTA scan above it."""
+    from oracle import flowcover_oracle as O
+
+    rng = np.random.default_rng(T + n)
+    A = 0.2 * rng.normal(size=(T, n, n)) - 0.5 * np.eye(n)
+    B = rng.normal(size=(T, n, m))
+    Q, R = np.eye(n), 0.1 * np.eye(m)
+    a = np.cumsum(rng.normal(scale=0.1, size=(T, n)), axis=0)
+    sol = fc.solve_flow_lqr(fc.LtvSystem(A=A, B=B, dt=0.05), a, fc.LqrWeights(Q=Q, R=R))
+    ref = O.solve_flow_lqr(A, B, 0.05, a, Q, R)
+    assert rel_inf(sol.v_star, ref["v"]) <= 1e-9
+    assert rel_inf(sol.z, ref["z"]) <= 1e-9
+    assert sol.cost == pytest.approx(ref["cost"], rel=1e-9)
+
+
 def dense_solution(A, B, dt, a, Q, R):  # the normal-equation oracle of test_lqr.py:44-63
     T, n, _ = A.shape
     m = B.shape[2]
