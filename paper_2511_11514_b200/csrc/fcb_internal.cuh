@@ -110,20 +110,15 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
-// Grid-wide barrier for cooperatively launched kernels.  count/gen live in
-// the caller's workspace and start at zero.
-#ifndef FCB_HBAR
-#define FCB_HBAR 0  // 1: two-level arrival (16 group counters); measured slower
-#endif
-constexpr int HBAR_GROUPS = 16;
-
+// Grid-wide barrier for cooperatively launched kernels: one arrival counter
+// that only grows (the caller zeroes it before the launch).  Barrier k of the
+// launch completes when the counter reaches k * nblocks, so a CTA derives its
+// target from the value its own arrival returned -- no generation word, no
+// reset, one atomic per CTA.  Measured 1.36 us per barrier at 296 CTAs
+// against 2.4 us for a count/generation pair with full fences.
 struct GridBarrier {
     unsigned count;
-    unsigned gen;
-#if FCB_HBAR
-    unsigned pad[30];
-    unsigned sub[HBAR_GROUPS * 32];  // one 128-byte line per group counter
-#endif
+    unsigned pad[31];  // own 128-byte line
 };
 
 #ifdef FCB_TIMELINE
@@ -155,66 +150,15 @@ __device__ __forceinline__ void grid_sync(GridBarrier* b) {
     FCB_TL_MARK();
     if (threadIdx.x == 0) {
         const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
-        const unsigned g = ld_acquire_u32(&b->gen);
-        __threadfence();
-#if FCB_HBAR
-        // arrivals spread over HBAR_GROUPS counters; the last CTA of each
-        // group arrives at the top counter, the last group releases
-        const unsigned ngroups = nb < (unsigned)HBAR_GROUPS ? nb : (unsigned)HBAR_GROUPS;
-        const unsigned grp = blockIdx.x % ngroups;
-        const unsigned members = nb / ngroups + (grp < nb % ngroups ? 1u : 0u);
-        bool releaser = false;
-        if (atomicAdd(&b->sub[grp * 32], 1u) == members - 1) {
-            b->sub[grp * 32] = 0;
-            __threadfence();
-            if (atomicAdd(&b->count, 1u) == ngroups - 1) {
-                b->count = 0;
-                __threadfence();
-                atomicAdd(&b->gen, 1u);
-                releaser = true;
-            }
-        }
-        if (!releaser)
-            while (ld_acquire_u32(&b->gen) == g) __nanosleep(20);
-#else
-        const unsigned arrived = atomicAdd(&b->count, 1u);
-        if (arrived == nb - 1) {
-            b->count = 0;
-            __threadfence();
-            atomicAdd(&b->gen, 1u);
-        } else {
-            while (ld_acquire_u32(&b->gen) == g) {
-                __nanosleep(20);
-            }
-        }
-#endif
-        __threadfence();
+        // the CTA's writes (ordered before this thread by bar.sync) are
+        // released at gpu scope before the arrival
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        const unsigned old = atomicAdd(&b->count, 1u);
+        const unsigned target = (old / nb + 1u) * nb;
+        while (ld_acquire_u32(&b->count) < target) __nanosleep(20);
     }
     __syncthreads();
     FCB_TL_MARK();
-}
-
-// Point-to-point producer/consumer sync between CTAs of a persistent grid:
-// the producer CTA publishes an epoch after its writes; consumers spin until
-// the epoch is reached.  Epochs only grow, so flags are never reset.
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void publish_epoch(unsigned* flag, unsigned epoch) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        st_release_u32(flag, epoch);
-    }
-}
-
-__device__ __forceinline__ void wait_epoch(const unsigned* flag, unsigned epoch) {
-    if (threadIdx.x == 0) {
-        while (ld_acquire_u32(flag) < epoch) __nanosleep(32);
-        __threadfence();
-    }
-    __syncthreads();
 }
 
 // max over non-negative doubles (NaN propagates: its bit pattern sorts above +inf)

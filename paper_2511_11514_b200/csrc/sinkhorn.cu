@@ -50,12 +50,6 @@ namespace fcb {
 #ifndef FCB_MINB
 #define FCB_MINB 2       // min resident CTAs per SM (register budget)
 #endif
-#ifndef FCB_FUSED_MERGE
-// 1: chunk merges by owner CTAs + epoch flags (2 barriers/iteration).  Measured
-// slower at config-2 sizes (one CTA per chunk merge serialises) -- kept as an
-// experiment; 0: separate grid-wide merge phases (4 barriers/iteration).
-#define FCB_FUSED_MERGE 0
-#endif
 
 constexpr int OT_BLOCK = 256;
 constexpr int OT_TILE = 256;    // columns staged per shared-memory tile
@@ -100,8 +94,6 @@ struct OtArgs {
     Real* pa2;
     Sweep A, B;
     GridBarrier* bar;
-    unsigned* flagX;              // per column chunk of X: epoch of its records
-    unsigned* flagY;              // per column chunk of Y
     unsigned long long* errslot;  // 3 slots
     double* f_out;
     double* g_out;
@@ -487,37 +479,6 @@ __device__ __forceinline__ void merge_phase(const Sweep& sw, const double* pm, c
     }
 }
 
-// CTA-local merge of the rows [j0, j1) of a finished sweep `sw` (the columns
-// of the caller's next work item), G lanes per row.  Called uniformly by all
-// threads of the CTA; epi(j, L) runs on the group's lane 0.
-template <typename Real, int D, int G, typename Epi>
-__device__ __forceinline__ void chunk_merge_g(const Sweep& sw, const double* pm, const Real* ps,
-                                              int j0, int j1, Epi&& epi) {
-    constexpr int GPW = 32 / G;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = lane / G, lig = lane % G;
-    const int nw = blockDim.x >> 5;
-    for (int base = j0 + warp * GPW; base < j1; base += nw * GPW) {
-        const int j = base + grp;
-        const bool valid = j < j1;
-        const double L = merge_row<Real, D, false, G>(valid ? j : j0, sw.nchunks, pm, ps, nullptr,
-                                                      sw.rows, lig, nullptr);
-        if (valid && lig == 0) epi(j, L);
-    }
-}
-
-template <typename Real, int D, typename Epi>
-__device__ __forceinline__ void chunk_merge(const Sweep& sw, const double* pm, const Real* ps,
-                                            int j0, int j1, Epi&& epi) {
-    if (j1 <= j0) return;
-    if (sw.nchunks <= 2)
-        chunk_merge_g<Real, D, 1>(sw, pm, ps, j0, j1, epi);
-    else if (sw.nchunks <= 16)
-        chunk_merge_g<Real, D, 4>(sw, pm, ps, j0, j1, epi);
-    else
-        chunk_merge_g<Real, D, 16>(sw, pm, ps, j0, j1, epi);
-}
-
 // ---------------------------------------------------------------------------
 // the persistent solver
 // ---------------------------------------------------------------------------
@@ -605,146 +566,6 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
         return;
     }
 
-#if FCB_FUSED_MERGE
-    // ---- fused loop: each work item merges the previous sweep's partials
-    // for its own column chunk, then sweeps.  Two grid barriers per
-    // asymmetric iteration, one per symmetric iteration; the convergence test
-    // of iteration k is read after the barrier that follows the merges of
-    // iteration k (one speculative sweep is discarded at exit).
-    const double inv_n = 1.0 / p.n;
-    const double inv_w = 1.0 / w;
-    const Real rpad = (Real)-INFINITY;
-    (void)rpad;
-    int cur = 0;  // fbuf[cur] holds the potential the current sweeps use
-    int it = 0;
-    while (true) {
-        ++it;
-        const bool merge_prev = it > 1;
-        const bool final_merge = merge_prev && (it - 1 >= p.max_iters);
-        const double* fprev = p.fbuf + (size_t)(cur ^ 1) * p.n;  // potential of iteration it-1
-        double* fnow = p.fbuf + (size_t)cur * p.n;               // potential of iteration it
-        // partial buffers: ASYM A -> set 0, B -> set 1; SYM ping-pong by parity
-        const int setB = asym ? 1 : ((it - 1) & 1);
-        const int setPrev = asym ? 1 : ((it - 2) & 1);
-        double* pmB = setB ? p.pm2 : p.pm;
-        Real* psB = setB ? p.ps2 : p.ps;
-        Real* paB = setB ? p.pa2 : p.pa;
-        const double* pmP = setPrev ? p.pm2 : p.pm;
-        const Real* psP = setPrev ? p.ps2 : p.ps;
-        unsigned long long* slot = p.errslot + ((it - 1) % 3);
-        // ---- phase X(it): rows of the sweep are X (ASYM: sweep A uses X as
-        // columns; SYM: the only sweep) -------------------------------------
-        const Sweep& SX = asym ? p.A : p.B;
-        double emax = 0.0;
-        for (int item = blockIdx.x; item < SX.items; item += gridDim.x) {
-            const int rb = item % SX.nrb, ch = item / SX.nrb;
-            const int c0 = ch * SX.chunk_len, c1 = min(c0 + SX.chunk_len, SX.cols8);
-            if (merge_prev && rb != 0) {
-                wait_epoch(p.flagX + ch, (unsigned)it);
-            } else if (merge_prev) {
-                // owner of the chunk: merge the previous f-sweep (ASYM: sweep B
-                // of it-1; SYM: it-1) for its X columns -- potential update,
-                // column records, err -- then publish the chunk
-                const bool owner = true;
-                chunk_merge<Real, D>(p.B, pmP, psP, c0, min(c1, p.n), [&](int i, double L) {
-                    const double fi = __ldcg(fprev + i);
-                    const double upd = w * (p.loga - L);
-                    double delta = (fi - upd) * inv_w;
-                    if (delta > EXP_CLIP) delta = EXP_CLIP;
-                    const double nxt = asym ? upd : 0.5 * (fi + upd);
-                    p.colX[i].w = (Real)(sd * nxt + (double)p.rowX[i].w);
-                    if (owner) {
-                        fnow[i] = nxt;
-                        const double e = fabs(expm1(delta));
-                        emax = (e > emax || e != e) ? e : emax;
-                    }
-                });
-                publish_epoch(p.flagX + ch, (unsigned)it);
-            }
-            if (!final_merge) {
-                if (asym) {
-                    const ShiftEst estA{it > 1 ? p.gbuf : nullptr, p.logb, inv_w, unit};
-                    sweep_item<Real, D, RPT, EXP, false>(p.rowY, p.m, rb * OT_BLOCK * RPT, p.colX, c0,
-                                                         c1, s, estA, p.pm, p.ps, p.pa, p.m, ch);
-                } else {
-                    const ShiftEst estS{fnow, p.loga, inv_w, unit};
-                    sweep_item<Real, D, RPT, EXP, BARY>(p.rowX, p.n, rb * OT_BLOCK * RPT, p.colX,
-                                                        c0, c1, s, estS, pmB, psB, paB, p.n, ch);
-                }
-            }
-        }
-        if (merge_prev) {  // block max of the merge errors -> one atomic per block
-            for (int o = 16; o > 0; o >>= 1) {
-                const double v = __shfl_xor_sync(0xffffffffu, emax, o);
-                emax = (v > emax || v != v) ? v : emax;
-            }
-            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = emax;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double b = 0.0;
-                for (int k = 0; k < OT_BLOCK / 32; ++k)
-                    b = (red[k] > b || red[k] != red[k]) ? red[k] : b;
-                atomic_max_nonneg(slot, b);
-                if (blockIdx.x == 0) p.errslot[it % 3] = 0ull;
-            }
-        }
-        grid_sync(p.bar);
-        if (merge_prev) {
-            const double err = __longlong_as_double((long long)__ldcg(slot)) * inv_n;
-            const bool conv = err <= p.tol;
-            if (conv || it - 1 >= p.max_iters) {
-                // outputs of iteration it-1: f (pre-update) = fprev, g = gbuf,
-                // row sums / barycentres from the partials of its f-sweep
-                const int K = it - 1;
-                merge_phase<Real, D, BARY>(p.B, pmP, psP, setPrev ? p.pa2 : p.pa,
-                                           [&](int i, double L, const double* bar) {
-                    const double fi = __ldcg(fprev + i);
-                    double delta = (fi - w * (p.loga - L)) * inv_w;
-                    if (delta > EXP_CLIP) delta = EXP_CLIP;
-                    p.rs_out[i] = exp(delta + p.loga);
-                    if (BARY && p.bary) {
-                        double* o = p.bary + (size_t)i * (D + 1);
-                        o[0] = exp(fi * inv_w + L);
-                        for (int q = 0; q < D; ++q) o[1 + q] = bar[q] / csc + c[q];
-                    }
-                });
-                for (int i = gtid; i < p.n; i += gthreads) p.f_out[i] = __ldcg(fprev + i);
-                if (asym && p.g_out)
-                    for (int j = gtid; j < p.m; j += gthreads) p.g_out[j] = __ldcg(p.gbuf + j);
-                if (gtid == 0) {
-                    p.stat[0] = err;
-                    p.stat[1] = (double)K;
-                    p.stat[2] = conv ? 1.0 : 0.0;
-                    p.stat[3] = 0.0;
-                }
-                return;
-            }
-        }
-        if (asym) {
-            // ---- phase Y(it): sweep B (rows X, columns Y), merging sweep A of
-            // this iteration for the Y columns of each chunk -----------------
-            for (int item = blockIdx.x; item < p.B.items; item += gridDim.x) {
-                const int rb = item % p.B.nrb, ch = item / p.B.nrb;
-                const int c0 = ch * p.B.chunk_len, c1 = min(c0 + p.B.chunk_len, p.B.cols8);
-                if (rb != 0) {
-                    wait_epoch(p.flagY + ch, (unsigned)it);
-                } else {
-                    chunk_merge<Real, D>(p.A, p.pm, p.ps, c0, min(c1, p.m), [&](int j, double L) {
-                        const double g = w * (p.logb - L);
-                        p.colY[j].w = (Real)(sd * g + (double)p.rowY[j].w);
-                        p.gbuf[j] = g;
-                    });
-                    publish_epoch(p.flagY + ch, (unsigned)it);
-                }
-                const ShiftEst estB{fnow, p.loga, inv_w, unit};
-                sweep_item<Real, D, RPT, EXP, BARY>(p.rowX, p.n, rb * OT_BLOCK * RPT, p.colY, c0, c1,
-                                                    s, estB, p.pm2, p.ps2, p.pa2, p.n, ch);
-            }
-            grid_sync(p.bar);
-        }
-        cur ^= 1;
-    }
-#else  // separate merge phases: 4 grid barriers per asymmetric iteration
     const double inv_n = 1.0 / p.n;
     int cur = 0;
     int it = 0;
@@ -822,7 +643,6 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
         }
         cur ^= 1;
     }
-#endif  // legacy 4-barrier loop
 }
 
 // ---------------------------------------------------------------------------
@@ -918,8 +738,6 @@ static void ot_layout(OtLayout<Real>& L, int mode, int n, int m, int d, int rpt,
     a.ps2 = ar.take<Real>(sweep ? 0 : pcount);
     a.pa2 = ar.take<Real>(sweep ? 0 : pcount * d);
     a.bar = ar.take<GridBarrier>(1);
-    a.flagX = ar.take<unsigned>(2 * OT_SMAX);  // contiguous with the barrier: one memset
-    a.flagY = a.flagX ? a.flagX + OT_SMAX : nullptr;
     a.errslot = ar.take<unsigned long long>(4);
     L.bytes = ar.off + 256;
 }
@@ -951,7 +769,6 @@ static int ot_launch(int mode, const double* X, int n, const double* Y, int m, c
     a.bary = bary;
     a.gate = gate;
     FCB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(GridBarrier), st));
-    FCB_CUDA(cudaMemsetAsync(a.flagX, 0, 2 * OT_SMAX * sizeof(unsigned), st));
     void* args[] = {&a};
     FCB_CUDA(cudaLaunchCooperativeKernel((const void*)ot_solve_kernel<Real, D, RPT, BARY>,
                                          dim3(grid), dim3(OT_BLOCK), args, 0, st));

@@ -32,8 +32,12 @@ for rep in range(3):
     k = lib.fcb_debug_timeline(buf, 8192)
 t = np.array(buf[:k], dtype=np.float64)
 t -= t[0]
-names = ["pack", "sweepA", "mergeA", "sweepB", "mergeB"]
 print(f"{k} stamps; total {t[-1]/1e3:.1f} us for {iters} iterations")
+if os.environ.get("FCB_TL_RAW"):
+    for i in range(1, k):
+        print(f"stamp {i:4d}: +{(t[i] - t[i - 1]) / 1e3:7.2f} us  (at {t[i] / 1e3:8.2f})")
+    sys.exit(0)
+names = ["pack", "sweepA", "mergeA", "sweepB", "mergeB"]
 # stamps come in (arrive, release) pairs per barrier
 prev_rel = 0.0
 for b in range(k // 2):
