@@ -118,7 +118,9 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 // against 2.4 us for a count/generation pair with full fences.
 struct GridBarrier {
     unsigned count;
-    unsigned pad[31];  // own 128-byte line
+    unsigned pad[31];   // own 128-byte line
+    unsigned work;      // dynamic work-item counter (grows across phases)
+    unsigned pad2[31];
 };
 
 #ifdef FCB_TIMELINE

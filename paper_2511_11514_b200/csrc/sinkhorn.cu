@@ -35,15 +35,13 @@
 #include "fcb_internal.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
 namespace fcb {
 
 // Tuning knobs (compile-time; see scripts/tune_ot.sh)
-#ifndef FCB_SMEM_TILE
-#define FCB_SMEM_TILE 1  // stage column records through shared memory
-#endif
 #ifndef FCB_TILE
 #define FCB_TILE 512     // columns per shared-memory tile
 #endif
@@ -52,7 +50,6 @@ namespace fcb {
 #endif
 
 constexpr int OT_BLOCK = 256;
-constexpr int OT_TILE = 256;    // columns staged per shared-memory tile
 constexpr int OT_SUB = 8;       // columns per register sub-tile
 constexpr int OT_SMAX = 96;     // max column chunks per sweep
 constexpr int OT_MIN_CHUNK = 64;
@@ -236,11 +233,64 @@ __device__ __forceinline__ Vec4<Real> load_col(const Vec4<Real>* p) {
     return Vec4<Real>{__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3)};
 }
 
+// Column record sources of a sweep.  PlainCols reads packed records;
+// MergedCols (sweep B of the asymmetric solve) folds the previous sweep's
+// merge into the tile staging: the potential of column j, g_j = w (log b -
+// LSE_j), is combined from sweep A's chunk partials of row j right where the
+// record is needed -- no merge phase, no grid barrier between the sweeps.
+// Every CTA combines the partials in the same order, so all copies of g_j
+// are bit-identical; the row-block-0 items also store g.
+template <typename Real>
+struct PlainCols {
+    const Vec4<Real>* cols;
+    __device__ __forceinline__ Vec4<Real> operator()(int j) const { return load_col(cols + j); }
+    __device__ __forceinline__ PlainCols for_block(int) const { return *this; }
+};
+
+template <typename Real>
+struct MergedCols {
+    const Vec4<Real>* colY;  // packed coordinates (.w unused)
+    const Vec4<Real>* rowY;  // .w: row constant of Y
+    const double* pm;        // sweep A partials [nch][ldp]
+    const Real* ps;
+    int nch, ldp, m;
+    double w, logb, sd;
+    double* gbuf;            // g store (row-block-0 items only)
+    double* gout;
+    __device__ __forceinline__ Vec4<Real> operator()(int j) const {
+        Vec4<Real> c = load_col(colY + j);
+        if (j >= m) return c;  // padding record (w = -inf)
+        double M = -INFINITY, S = 0.0;
+        for (int k = 0; k < nch; ++k) {
+            const double mk = __ldcg(pm + (size_t)k * ldp + j);
+            const double sk = (double)__ldcg(ps + (size_t)k * ldp + j);
+            if (mk > M) {
+                const double sc = (S > 0.0) ? dexpu<Real>(M - mk) : 0.0;
+                S = S * sc + sk;
+                M = mk;
+            } else {
+                S += sk * dexpu<Real>(mk - M);
+            }
+        }
+        const double L = (M + Units<Real>::logu(S)) / Units<Real>::unit;
+        const double g = w * (logb - L);
+        if (gout) gout[j] = g;
+        c.w = (Real)(sd * g + (double)__ldcg(reinterpret_cast<const Real*>(rowY + j) + 3));
+        return c;
+    }
+    __device__ __forceinline__ MergedCols for_block(int rb) const {
+        MergedCols c = *this;
+        c.gout = (rb == 0) ? gbuf : nullptr;
+        return c;
+    }
+};
+
 // One work item: RPT rows per thread x columns [c0, c1) (c1 - c0 a multiple
 // of OT_SUB).  Emits the partial (shift, sum[, moments]) of every row.
-template <typename Real, int D, int RPT, bool EXP, bool BARY>
+template <typename Real, int D, int RPT, bool EXP, bool BARY, class Cols>
 __device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, int nrows, int row0,
-                                           const Vec4<Real>* __restrict__ cols, int c0, int c1,
+                                           const Cols& cols, int c0, int c1,
+                                           Vec4<Real>* __restrict__ s_tile,
                                            Real s, const ShiftEst& est, double* __restrict__ pm,
                                            Real* __restrict__ ps, Real* __restrict__ pa, int ldp,
                                            int chunk) {
@@ -263,14 +313,12 @@ __device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, 
 #pragma unroll
         for (int k = 0; k < D; ++k) acc[r][k] = 0;
     }
-#if FCB_SMEM_TILE
     // columns staged through shared memory (coalesced cooperative loads,
     // LDS.128 broadcast reads)
-    __shared__ Vec4<Real> s_tile[FCB_TILE];
     for (int t0 = c0; t0 < c1; t0 += FCB_TILE) {
     const int tlen = min(FCB_TILE, c1 - t0);
     __syncthreads();
-    for (int k = tid; k < tlen; k += OT_BLOCK) s_tile[k] = load_col(cols + t0 + k);
+    for (int k = tid; k < tlen; k += OT_BLOCK) s_tile[k] = cols(t0 + k);
     __syncthreads();
     for (int c = 0; c < tlen; c += OT_SUB) {
         Real cy[OT_SUB][D], cw[OT_SUB];
@@ -281,25 +329,6 @@ __device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, 
             for (int q = 0; q < D; ++q) cy[k][q] = vget(v, q);
             cw[k] = v.w;
         }
-#else
-    // register double buffer of column records
-    Vec4<Real> nxt[OT_SUB];
-#pragma unroll
-    for (int k = 0; k < OT_SUB; ++k) nxt[k] = load_col(cols + c0 + k);
-    {
-    for (int c = c0; c < c1; c += OT_SUB) {
-        Real cy[OT_SUB][D], cw[OT_SUB];
-#pragma unroll
-        for (int k = 0; k < OT_SUB; ++k) {
-#pragma unroll
-            for (int q = 0; q < D; ++q) cy[k][q] = vget(nxt[k], q);
-            cw[k] = nxt[k].w;
-        }
-        if (c + OT_SUB < c1) {
-#pragma unroll
-            for (int k = 0; k < OT_SUB; ++k) nxt[k] = load_col(cols + c + OT_SUB + k);
-        }
-#endif
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
             Real t[OT_SUB], e[OT_SUB];
@@ -351,7 +380,7 @@ __device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, 
             }
         }
     }
-    }  // tile loop (FCB_SMEM_TILE) / buffer scope
+    }  // tile loop
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
         const int i = row0 + r * OT_BLOCK + tid;
@@ -366,18 +395,35 @@ __device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, 
     }
 }
 
-template <typename Real, int D, int RPT, bool EXP, bool BARY>
+// All items of a sweep.  Item blockIdx.x is static (no atomic before the
+// first item); the rest are handed out dynamically, so CTAs that run faster
+// (an SM shared with a slower neighbour, earlier start) take more items.  The
+// work counter only grows: a sweep with `items` items consumes exactly
+// `items` counter values (every CTA that ran a static item makes one failing
+// grab), so the caller advances base by items.  The next item is grabbed
+// while the current one runs.
+template <typename Real, int D, int RPT, bool EXP, bool BARY, class Cols>
 __device__ __forceinline__ void run_sweep(const Sweep& sw, const Vec4<Real>* rows,
-                                          const Vec4<Real>* cols, Real s, const ShiftEst& est,
-                                          double* pm, Real* ps, Real* pa) {
+                                          const Cols& cols, Real s, const ShiftEst& est,
+                                          double* pm, Real* ps, Real* pa, unsigned* work,
+                                          unsigned base, Vec4<Real>* s_tile) {
+    __shared__ int s_item;
     const int ldp = sw.rows;
-    for (int item = blockIdx.x; item < sw.items; item += gridDim.x) {
+    const int grid = gridDim.x;
+    int item = blockIdx.x;
+    while (item < sw.items) {
+        unsigned nxt = 0;
+        if (threadIdx.x == 0) nxt = atomicAdd(work, 1u);
         const int rb = item % sw.nrb;
         const int ch = item / sw.nrb;
         const int c0 = ch * sw.chunk_len;
         const int c1 = min(c0 + sw.chunk_len, sw.cols8);
-        sweep_item<Real, D, RPT, EXP, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT, cols, c0, c1, s, est,
-                                            pm, ps, pa, ldp, ch);
+        sweep_item<Real, D, RPT, EXP, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT, cols.for_block(rb),
+                                            c0, c1, s_tile, s, est, pm, ps, pa, ldp, ch);
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = grid + (int)(nxt - base);
+        __syncthreads();
+        item = s_item;
     }
 }
 
@@ -486,6 +532,7 @@ template <typename Real, int D, int RPT, bool BARY>
 __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Real> p) {
     constexpr bool EXP = (sizeof(Real) == 4);
     __shared__ double red[32];
+    __shared__ Vec4<Real> s_tile[FCB_TILE];  // column records of the current tile
 
     if (p.gate && *((volatile const int*)p.gate) != 0) return;
 
@@ -551,7 +598,8 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
     const double unit = Units<Real>::unit;
     if (sweep_only) {
         const ShiftEst none{nullptr, 0.0, 0.0, unit};
-        run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, p.colY, s, none, p.pm, p.ps, p.pa);
+        run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colY}, s, none, p.pm, p.ps,
+                                           p.pa, &p.bar->work, 0u, s_tile);
         grid_sync(p.bar);
         double* out = p.f_out;
         double* bo = p.bary;
@@ -567,6 +615,7 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
     }
 
     const double inv_n = 1.0 / p.n;
+    unsigned wbase = 0;  // work-counter base of the next sweep
     int cur = 0;
     int it = 0;
     while (true) {
@@ -574,28 +623,36 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
         const double* fcur = p.fbuf + (size_t)cur * p.n;
         double* fnxt = p.fbuf + (size_t)(cur ^ 1) * p.n;
         unsigned long long* slot = p.errslot + (it % 3);
+        // sweep partials: ASYM sweep A -> set 1, sweep B -> set 2 (sweep B
+        // reads set 1 while it runs); SYM -> set 1
+        double* pmB = asym ? p.pm2 : p.pm;
+        Real* psB = asym ? p.ps2 : p.ps;
+        Real* paB = asym ? p.pa2 : p.pa;
+        const ShiftEst estB{fcur, p.loga, 1.0 / w, unit};
         if (asym) {
             // ---- sweep A: rows Y, columns X (potential f) --------------
             // shift estimate: g of the previous iteration (none at it == 1)
             const ShiftEst estA{it > 1 ? p.gbuf : nullptr, p.logb, 1.0 / w, unit};
-            run_sweep<Real, D, RPT, EXP, false>(p.A, p.rowY, p.colX, s, estA, p.pm, p.ps, p.pa);
+            run_sweep<Real, D, RPT, EXP, false>(p.A, p.rowY, PlainCols<Real>{p.colX}, s, estA, p.pm,
+                                                p.ps, p.pa, &p.bar->work, wbase, s_tile);
+            wbase += (unsigned)p.A.items;
             grid_sync(p.bar);
-            // ---- merge A: g = w (log b - Lg) ---------------------------
-            merge_phase<Real, D, false>(p.A, p.pm, p.ps, p.pa, [&](int j, double L, const double*) {
-                const double g = w * (p.logb - L);
-                p.gbuf[j] = g;
-                p.colY[j].w = (Real)(sd * g + (double)p.rowY[j].w);
-            });
-            grid_sync(p.bar);
+            // ---- sweep B: rows X, columns Y with g = w (log b - LSE_A)
+            // merged from sweep A's partials while staging the tiles -----
+            const MergedCols<Real> colsB{p.colY, p.rowY, p.pm, p.ps, p.A.nchunks, p.A.rows, p.m,
+                                         w, p.logb, sd, p.gbuf, nullptr};
+            run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, colsB, s, estB, pmB, psB, paB,
+                                               &p.bar->work, wbase, s_tile);
+        } else {
+            // ---- SYM: rows X, columns X --------------------------------------
+            run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colX}, s, estB, pmB,
+                                               psB, paB, &p.bar->work, wbase, s_tile);
         }
-        // ---- sweep B: rows X, columns Y (ASYM, potential g) or X (SYM) --
-        const ShiftEst estB{fcur, p.loga, 1.0 / w, unit};
-        run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, asym ? p.colY : p.colX, s, estB, p.pm, p.ps,
-                                           p.pa);
+        wbase += (unsigned)p.B.items;
         grid_sync(p.bar);
         // ---- merge B ------------------------------------------------------
         double emax = 0.0;
-        merge_phase<Real, D, BARY>(p.B, p.pm, p.ps, p.pa, [&](int i, double L, const double* bar) {
+        merge_phase<Real, D, BARY>(p.B, pmB, psB, paB, [&](int i, double L, const double* bar) {
             const double fi = __ldcg(fcur + i);
             const double upd = w * (p.loga - L);  // f_new (ASYM) / target (SYM)
             double delta = (fi - upd) / w;
@@ -656,7 +713,20 @@ static Sweep plan_sweep(int rows, int cols, int rpt, int grid) {
     const int br = OT_BLOCK * rpt;
     s.nrb = (rows + br - 1) / br;
     const int max_chunks = std::max(1, std::min(OT_SMAX, s.cols8 / OT_MIN_CHUNK));
-    // pick the chunk count that best fills whole waves of the persistent grid
+    const double pairs = (double)rows * (double)cols;
+    if (pairs > 4e5 * grid) {
+        // large sweeps: several items per CTA (~200k pairs each, at most 8 per
+        // CTA), balanced at run time by the dynamic item counter
+        const double target = std::min(8.0 * grid, pairs / 2e5);
+        const int k = std::max(1, std::min(max_chunks, (int)std::ceil(target / s.nrb)));
+        int cl = (s.cols8 + k - 1) / k;
+        cl = (cl + OT_SUB - 1) / OT_SUB * OT_SUB;
+        s.chunk_len = cl;
+        s.nchunks = (s.cols8 + cl - 1) / cl;
+        s.items = s.nrb * s.nchunks;
+        return s;
+    }
+    // small sweeps: the chunk count that best fills whole waves of the grid
     int best = 1;
     double best_eff = -1.0;
     for (int k = 1; k <= max_chunks; ++k) {
