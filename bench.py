@@ -17,10 +17,11 @@ value   inputs resident in HBM (targets pre-staged), CUDA events on the
         launching stream over the K timed steps, max over ranks.
 e2e     the public plan() with host numpy inputs (uploads + result
         download inside the timed region).
-roofline  the dominant kernel (the persistent asymmetric Sinkhorn solve)
-        replayed live on the last iteration's inputs, achieved pair-evals/s
-        (= MUFU.EX2/s, one exp per pair) vs the MUFU.EX2 peak measured by the
-        probe kernel in this run.
+roofline  the dominant kernel (flow_kernel, one launch per planner
+        iteration), timed live inside the timed region by the planner's CUDA
+        events around each launch: executed pair-evals/s (= MUFU.EX2/s, one
+        exp2 per pair) vs the MUFU.EX2 peak measured by the probe kernel in
+        this run; traffic from the committed ncu capture.
 cpu_baseline  the oracle port of the reference (numpy float64, row-chunked
         thread pool as in the reference) on this host's cores, on a bounded
         sample of the same workload (the first outer iterations).
@@ -143,43 +144,16 @@ def measure_peak(torch, lib, iters=4096):
     return res
 
 
-def roofline_replay(torch, fc, X_last: np.ndarray, Y: np.ndarray, reps: int = 20):
-    """Time the dominant kernel (asymmetric solve, fp32) on the last iterate."""
-    from paper_2511_11514_b200 import _dev, _lib, _precision
-    from paper_2511_11514_b200.sinkhorn import _resolve_on_device
-
-    n, d = X_last.shape
-    m = Y.shape[0]
-    prec = _precision.pick("auto", n * max(n, m), 1e-6)
-    dev = _dev.require_cuda()
-    Xd, Yd = _dev.f64(X_last, dev), _dev.f64(Y, dev)
-    scal = _resolve_on_device(_lib.FCB_OT_ASYM, prec, Xd, n, Yd, m, d, 0.0)
-    lib = _lib.load()
-    f, g, rs = _dev.empty((n,)), _dev.empty((m,)), _dev.empty((n,))
-    stat, bary = _dev.empty((4,)), _dev.empty((n, d + 1))
-    ws = _dev.Workspace.get(lib.fcb_ot_workspace_bytes(_lib.FCB_OT_ASYM, prec, n, m, d), "roof")
-    # fixed inner-iteration budget: tol below any reachable error
-    iters = 10
-
-    def launch():
-        _lib.call("fcb_ot_solve", _lib.FCB_OT_ASYM, prec, _dev.ptr(Xd), n, _dev.ptr(Yd), m, d,
-                  _dev.ptr(scal), iters, 1e-300, None, _dev.ptr(f), _dev.ptr(g), _dev.ptr(rs),
-                  _dev.ptr(stat), _dev.ptr(bary), None, _dev.ptr(ws), ws.numel(), _dev.stream())
-
-    for _ in range(3):
-        launch()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        launch()
-    e1.record()
-    e1.synchronize()
-    per_launch = e0.elapsed_time(e1) * 1e-3 / reps
-    used = int(stat[1].item())
-    pairs = 2.0 * used * n * m
-    return {"pairs_per_launch": pairs, "seconds_per_launch": per_launch,
-            "pairs_per_s": pairs / per_launch, "inner_iterations": used, "precision": prec}
+def load_traffic():
+    """dram bytes per flow_kernel launch from the committed ncu --set full
+    capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "flow_kernel_traffic.json")
+    try:
+        with open(path) as fh:
+            rec = json.load(fh)
+        return rec
+    except (OSError, ValueError):
+        return None
 
 
 def run_ours(args):
@@ -268,31 +242,40 @@ def run_ours(args):
     t_e2e = max_over_ranks(ee0.elapsed_time(ee1) * 1e-3)
     e2e_pairs_all = sum_over_ranks(e2e_pairs)
 
-    # ---- roofline of the dominant kernel (live replay) -------------------------
+    # ---- roofline of the dominant kernel (live, inside the timed region) -----
+    # Each planner iteration launches flow_kernel once (one-launch Sinkhorn
+    # flow); plan() brackets that launch with CUDA events on its stream, so the
+    # flow phase time of the timed steps is the kernel's device time (plus one
+    # 256-byte barrier memset per launch).  Algorithmic work: one exp2 per
+    # (query, source) pair of every executed LSE sweep.
     roof = None
     if rank == 0:
         peak = measure_peak(torch, lib)
-        X_last = runs[-1].result.trajectory.S[1:, :2].copy()
-        rr = roofline_replay(torch, fc, X_last, Y)
         ex2_peak = peak["ex2"]
+        t_flow = sum(r.result.phase_times.flow for r in runs)
+        t_total = sum(r.result.phase_times.total for r in runs)
+        n_launch = sum(r.result.iterations_used for r in runs)
+        achieved = pairs_local / max(t_flow, 1e-12)
+        tr = load_traffic()
         roof = {
             "bound": "mufu",
-            "kernel": "ot_solve_kernel<float,2,2,true> (persistent asymmetric Sinkhorn solve)",
-            "achieved": rr["pairs_per_s"] / 1e9,
+            "kernel": "flow_kernel<float,2,2> (one-launch Sinkhorn flow: omega, packs, "
+                      "asymmetric + self solves, envelope gradient)",
+            "achieved": achieved / 1e9,
             "peak": ex2_peak / 1e9,
             "unit": "Gexp/s",
-            "frac": rr["pairs_per_s"] / ex2_peak,
-            "traffic": None,
+            "frac": achieved / ex2_peak,
+            "traffic": (tr["dram_bytes_per_launch"] if tr else None),
+            "traffic_source": (tr["source"] if tr else None),
+            "algorithmic_bytes_per_launch": (tr["algorithmic_bytes_per_launch"] if tr else None),
             "peak_source": "measured MUFU.EX2 probe (fcb_peak_probe) in this run",
             "ffma_peak_Gops": peak["ffma"] / 1e9,
-            "algorithmic": "1 exp per pair; pairs/launch = 2*k*T*M",
-            "pairs_per_launch": rr["pairs_per_launch"],
-            "ms_per_launch": rr["seconds_per_launch"] * 1e3,
-            "share_of_step": None,
+            "algorithmic": "1 exp2 per pair; pairs/launch = 2*k_a*T*M + k_s*T^2 (executed)",
+            "launches": n_launch,
+            "pairs_per_launch": pairs_local / max(n_launch, 1),
+            "ms_per_launch": t_flow / max(n_launch, 1) * 1e3,
+            "share_of_step": t_flow / max(t_total, 1e-12),
         }
-        flow_phase = sum(r.result.phase_times.flow for r in runs) / max(
-            sum(r.result.phase_times.total for r in runs), 1e-12)
-        roof["flow_phase_share_of_step"] = flow_phase
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -528,25 +528,29 @@ __device__ __forceinline__ void merge_phase(const Sweep& sw, const double* pm, c
 // ---------------------------------------------------------------------------
 // the persistent solver
 // ---------------------------------------------------------------------------
-template <typename Real, int D, int RPT, bool BARY>
-__global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Real> p) {
+// Scalars of a solve: omega, the exponent scale s = unit / omega and the
+// centre (scal[] of resolve_omega, or computed in-kernel by the flow kernel).
+struct OtScal {
+    double w, sd, c[3];
+};
+
+__device__ __forceinline__ OtScal load_scal(const double* scal) {
+    return OtScal{scal[SC_OMEGA], scal[SC_S], {scal[SC_C], scal[SC_C + 1], scal[SC_C + 2]}};
+}
+
+// Phase 0: centred row records, column records with the folded potential f0
+// (nullable), padding, error slots.  Grid-strided; the caller syncs.
+template <typename Real, int D>
+__device__ __forceinline__ void pack_phase(const OtArgs<Real>& p, const OtScal& sc,
+                                           const double* f0) {
     constexpr bool EXP = (sizeof(Real) == 4);
-    __shared__ double red[32];
-    __shared__ Vec4<Real> s_tile[FCB_TILE];  // column records of the current tile
-
-    if (p.gate && *((volatile const int*)p.gate) != 0) return;
-
-    const double w = p.scal[SC_OMEGA];
-    const double sd = p.scal[SC_S];
-    const Real s = (Real)sd;
-    const double c[3] = {p.scal[SC_C], p.scal[SC_C + 1], p.scal[SC_C + 2]};
+    const double sd = sc.sd;
+    const double* c = sc.c;
     const int gthreads = gridDim.x * blockDim.x;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const bool asym = (p.mode == FCB_OT_ASYM);
     const bool sweep_only = (p.mode == FCB_OT_SWEEP);
     const double csc = EXP ? 2.0 * sd : 1.0;  // column coordinate scale
-
-    // ---- phase 0: packs -------------------------------------------------
     for (int i = gtid; i < p.n; i += gthreads) {
         Real xs[3] = {0, 0, 0};
         double nrm = 0.0;
@@ -558,7 +562,7 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
         const double rowc = EXP ? -sd * nrm : 0.0;
         p.rowX[i] = Vec4<Real>{xs[0], xs[1], xs[2], (Real)rowc};
         if (!sweep_only) {
-            const double f = p.f0 ? p.f0[i] : 0.0;
+            const double f = f0 ? f0[i] : 0.0;
             p.fbuf[i] = f;
             p.colX[i] = Vec4<Real>{(Real)(csc * (double)xs[0]), (Real)(csc * (double)xs[1]),
                                    (Real)(csc * (double)xs[2]), (Real)(sd * f + rowc)};
@@ -580,7 +584,7 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
             }
             const double rowc = EXP ? -sd * nrm : 0.0;
             if (asym) p.rowY[j] = Vec4<Real>{ys[0], ys[1], ys[2], (Real)rowc};
-            const double pot = sweep_only ? p.f0[j] : 0.0;
+            const double pot = sweep_only ? f0[j] : 0.0;
             p.colY[j] = Vec4<Real>{(Real)(csc * (double)ys[0]), (Real)(csc * (double)ys[1]),
                                    (Real)(csc * (double)ys[2]), (Real)(sd * pot + rowc)};
         }
@@ -593,29 +597,50 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
         p.errslot[1] = 0ull;
         p.errslot[2] = 0ull;
     }
-    grid_sync(p.bar);
+}
 
+// The SWEEP mode: one LSE pass of rows X over columns Y (potential f0).
+template <typename Real, int D, int RPT, bool BARY>
+__device__ __forceinline__ void sweep_only_pass(const OtArgs<Real>& p, const OtScal& sc,
+                                                Vec4<Real>* s_tile) {
+    constexpr bool EXP = (sizeof(Real) == 4);
+    const Real s = (Real)sc.sd;
+    const double* c = sc.c;
+    const double csc = EXP ? 2.0 * sc.sd : 1.0;
     const double unit = Units<Real>::unit;
-    if (sweep_only) {
-        const ShiftEst none{nullptr, 0.0, 0.0, unit};
-        run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colY}, s, none, p.pm, p.ps,
-                                           p.pa, &p.bar->work, 0u, s_tile);
-        grid_sync(p.bar);
-        double* out = p.f_out;
-        double* bo = p.bary;
-        merge_phase<Real, D, BARY>(p.B, p.pm, p.ps, p.pa, [&](int i, double L, const double* bar) {
-            out[i] = L;
-            if (BARY && bo) {  // weighted mean of the columns (M-shard combine)
-                double* o = bo + (size_t)i * (D + 1);
-                o[0] = 1.0;
-                for (int q = 0; q < D; ++q) o[1 + q] = bar[q] / csc + c[q];
-            }
-        });
-        return;
-    }
+    const ShiftEst none{nullptr, 0.0, 0.0, unit};
+    run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colY}, s, none, p.pm, p.ps,
+                                       p.pa, &p.bar->work, 0u, s_tile);
+    grid_sync(p.bar);
+    double* out = p.f_out;
+    double* bo = p.bary;
+    merge_phase<Real, D, BARY>(p.B, p.pm, p.ps, p.pa, [&](int i, double L, const double* bar) {
+        out[i] = L;
+        if (BARY && bo) {  // weighted mean of the columns (M-shard combine)
+            double* o = bo + (size_t)i * (D + 1);
+            o[0] = 1.0;
+            for (int q = 0; q < D; ++q) o[1 + q] = bar[q] / csc + c[q];
+        }
+    });
+}
 
+// The Sinkhorn iterations of an ASYM or SYM solve (after pack_phase and a
+// grid barrier) up to convergence or max_iters, then the outputs.  wbase:
+// work-counter base, carried across solves that share the barrier.
+template <typename Real, int D, int RPT, bool BARY>
+__device__ __forceinline__ void solve_loop(const OtArgs<Real>& p, const OtScal& sc, unsigned& wbase,
+                                           double* red, Vec4<Real>* s_tile) {
+    constexpr bool EXP = (sizeof(Real) == 4);
+    const double w = sc.w;
+    const double sd = sc.sd;
+    const Real s = (Real)sd;
+    const double* c = sc.c;
+    const int gthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool asym = (p.mode == FCB_OT_ASYM);
+    const double csc = EXP ? 2.0 * sd : 1.0;
+    const double unit = Units<Real>::unit;
     const double inv_n = 1.0 / p.n;
-    unsigned wbase = 0;  // work-counter base of the next sweep
     int cur = 0;
     int it = 0;
     while (true) {
@@ -699,6 +724,209 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
             return;
         }
         cur ^= 1;
+    }
+}
+
+template <typename Real, int D, int RPT, bool BARY>
+__global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Real> p) {
+    __shared__ double red[32];
+    __shared__ Vec4<Real> s_tile[FCB_TILE];  // column records of the current tile
+    if (p.gate && *((volatile const int*)p.gate) != 0) return;
+    const OtScal sc = load_scal(p.scal);
+    pack_phase<Real, D>(p, sc, p.f0);
+    grid_sync(p.bar);
+    if (p.mode == FCB_OT_SWEEP) {
+        sweep_only_pass<Real, D, RPT, BARY>(p, sc, s_tile);
+        return;
+    }
+    unsigned wbase = 0;
+    solve_loop<Real, D, RPT, BARY>(p, sc, wbase, red, s_tile);
+}
+
+// ---------------------------------------------------------------------------
+// sinkhorn_flow in one launch (sinkhorn.py:355-397): statistics and omega,
+// the packs of both problems, the asymmetric solve (X vs Y), the self term
+// (X vs X), the envelope gradient, warm state and planner hooks.  The grid
+// barrier and its work counter are shared by both solves.
+// ---------------------------------------------------------------------------
+template <typename Real>
+struct FlowArgs {
+    OtArgs<Real> a;  // X vs Y, centred on (mean X + mean Y) / 2
+    OtArgs<Real> b;  // X vs X, centred on mean X
+    double omega_fixed;
+    double* part;      // grid x 8 partial sums (X: sum, |x|^2; Y: same)
+    double* scal;      // [16] outputs (resolve_omega layout)
+    double* scal_self;
+    double* warm_f;    // warm state: read at the start, stored at the end
+    double* warm_p;
+    int* warm_valid;
+    double* flow;
+    double* fstat;
+    int* plan_state;
+    int iteration;
+    double* flow_log;
+    double conv_tol;
+    double* fin_part;  // grid
+};
+
+template <typename Real, int D, int RPT>
+__global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) flow_kernel(FlowArgs<Real> fa) {
+    __shared__ double red[32];
+    __shared__ double s_sum[8];
+    __shared__ Vec4<Real> s_tile[FCB_TILE];
+    const OtArgs<Real>& A = fa.a;
+    const OtArgs<Real>& B = fa.b;
+    if (fa.plan_state && *((volatile const int*)fa.plan_state) != 0) return;
+    const int gthreads = gridDim.x * blockDim.x;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = A.n, m = A.m;
+
+    // ---- statistics of X and Y -> omega and both centrings ----------------
+    {
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = gtid; i < n; i += gthreads) {
+            double sq = 0.0;
+            for (int k = 0; k < D; ++k) {
+                const double v = A.X[(size_t)i * D + k];
+                acc[k] += v;
+                sq += v * v;
+            }
+            acc[3] += sq;
+        }
+        for (int j = gtid; j < m; j += gthreads) {
+            double sq = 0.0;
+            for (int k = 0; k < D; ++k) {
+                const double v = A.Y[(size_t)j * D + k];
+                acc[4 + k] += v;
+                sq += v * v;
+            }
+            acc[7] += sq;
+        }
+        for (int k = 0; k < 8; ++k) {
+            const double r = block_sum<OT_BLOCK>(acc[k], red);
+            if (threadIdx.x == 0) fa.part[blockIdx.x * 8 + k] = r;
+        }
+    }
+    grid_sync(A.bar);
+    if (threadIdx.x < 32) {  // every CTA combines the partials in one fixed order
+        const int lane = threadIdx.x;
+        for (int k = 0; k < 8; ++k) {
+            double v = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(fa.part + b * 8 + k);
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) s_sum[k] = v;
+        }
+    }
+    __syncthreads();
+    double mx[3] = {0, 0, 0}, my[3] = {0, 0, 0}, dot = 0.0;
+    for (int k = 0; k < D; ++k) {
+        mx[k] = s_sum[k] / n;
+        my[k] = s_sum[4 + k] / m;
+        dot += mx[k] * my[k];
+    }
+    const double mx2 = s_sum[3] / n, my2 = s_sum[7] / m;
+    double w = fa.omega_fixed;
+    if (!(w > 0.0)) {  // resolve_omega "auto", sinkhorn.py:136-148
+        w = AUTO_OMEGA_FACTOR * (mx2 + my2 - 2.0 * dot);
+        if (!(w >= OMEGA_FLOOR)) w = (w != w) ? w : OMEGA_FLOOR;
+    }
+    const double unit = Units<Real>::unit;
+    OtScal scA{w, unit / w, {0, 0, 0}}, scB{w, unit / w, {0, 0, 0}};
+    for (int k = 0; k < D; ++k) {
+        scA.c[k] = 0.5 * (mx[k] + my[k]);
+        scB.c[k] = mx[k];
+    }
+    if (gtid == 0) {
+        for (double* sc : {fa.scal, fa.scal_self}) {
+            const bool self = sc == fa.scal_self;
+            sc[SC_OMEGA] = w;
+            sc[SC_S] = unit / w;
+            for (int k = 0; k < 3; ++k) {
+                sc[SC_C + k] = self ? scB.c[k] : scA.c[k];
+                sc[SC_MX + k] = mx[k];
+                sc[SC_MY + k] = my[k];
+            }
+            sc[SC_MX2] = mx2;
+            sc[SC_MY2] = my2;
+        }
+    }
+    // warm start: the previous flow's potentials when they were stored
+    const bool vf = fa.warm_valid && fa.warm_valid[0] != 0;
+    const bool vp = fa.warm_valid && fa.warm_valid[1] != 0;
+    pack_phase<Real, D>(A, scA, vf ? fa.warm_f : nullptr);
+    pack_phase<Real, D>(B, scB, vp ? fa.warm_p : nullptr);
+    grid_sync(A.bar);
+
+    unsigned wbase = 0;
+    solve_loop<Real, D, RPT, true>(A, scA, wbase, red, s_tile);
+    solve_loop<Real, D, RPT, true>(B, scB, wbase, red, s_tile);
+    grid_sync(A.bar);
+
+    // ---- finalize: FlowError test, envelope gradient, warm state ----------
+    const double ex = __ldcg(A.stat), ep = __ldcg(B.stat);
+    const double worst = (ex > ep || ex != ex) ? ex : ep;
+    const bool flow_error = worst > 100.0 * A.tol;
+    double norm_acc = 0.0;
+    if (!flow_error) {
+        for (int i = gtid; i < n; i += gthreads) {
+            const double* bx = A.bary + (size_t)i * (D + 1);
+            const double* bp = B.bary + (size_t)i * (D + 1);
+            const double rcx = __ldcg(A.rs_out + i), rux = __ldcg(bx);
+            const double rcp = __ldcg(B.rs_out + i), rup = __ldcg(bp);
+            double sq = 0.0;
+            for (int k = 0; k < D; ++k) {
+                const double x = A.X[(size_t)i * D + k];
+                const double ty = rux * __ldcg(bx + 1 + k);
+                const double px = rup * __ldcg(bp + 1 + k);
+                const double grad = 2.0 * (rcx * x - ty) - 2.0 * (rcp * x - px);
+                fa.flow[(size_t)i * D + k] = -grad;
+                sq += grad * grad;
+            }
+            norm_acc += sqrt(sq);
+            if (fa.warm_f) {
+                fa.warm_f[i] = __ldcg(A.f_out + i);
+                fa.warm_p[i] = __ldcg(B.f_out + i);
+            }
+        }
+    }
+    const double blk = block_sum<OT_BLOCK>(norm_acc, red);
+    if (threadIdx.x == 0) fa.fin_part[blockIdx.x] = blk;
+    grid_sync(A.bar);
+    if (blockIdx.x != 0) return;
+    double tsum = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += OT_BLOCK) tsum += __ldcg(fa.fin_part + b);
+    const double total = block_sum<OT_BLOCK>(tsum, red);
+    if (threadIdx.x == 0) {
+        const double mean_mag = total / n;
+        double* fs = fa.fstat;
+        fs[0] = worst;
+        fs[1] = (__ldcg(A.stat + 2) != 0.0 && __ldcg(B.stat + 2) != 0.0) ? 1.0 : 0.0;
+        fs[2] = flow_error ? 1.0 : 0.0;
+        fs[3] = flow_error ? NAN : mean_mag;
+        fs[4] = w;
+        fs[5] = __ldcg(A.stat + 1);
+        fs[6] = __ldcg(B.stat + 1);
+        fs[7] = 0.0;
+        if (!flow_error && fa.warm_valid) {
+            fa.warm_valid[0] = 1;
+            fa.warm_valid[1] = 1;
+        }
+        if (int* ps = fa.plan_state) {
+            if (flow_error) {
+                ps[FCB_STATE_STOP] = 2;
+                ps[FCB_STATE_STAGE] = 2;
+                ps[FCB_STATE_ITER] = fa.iteration;
+                ps[FCB_STATE_INDEX] = -1;
+            } else {
+                double* lg = fa.flow_log + 4 * (size_t)fa.iteration;
+                lg[0] = mean_mag;
+                lg[1] = fs[5];
+                lg[2] = fs[6];
+                lg[3] = worst;
+                ps[FCB_STATE_FLOWS] = fa.iteration + 1;
+                if (mean_mag < fa.conv_tol) ps[FCB_STATE_STOP] = 1;
+            }
+        }
     }
 }
 
@@ -977,94 +1205,6 @@ __global__ void ot_plan_kernel(const double* __restrict__ X, int n, const double
     }
 }
 
-// finalize of sinkhorn_flow: FlowError test, envelope gradient, warm state,
-// mean magnitude and the planner's convergence hook.  Multi-block; the last
-// block to finish sums the per-block magnitudes in block order (deterministic)
-// and runs the scalar epilogue.
-constexpr int FIN_BLOCK = 256;
-constexpr int FIN_GRID = 148;
-__global__ void __launch_bounds__(FIN_BLOCK)
-    flow_finalize_kernel(const double* __restrict__ X, int n, int d, double tol,
-                         const double* __restrict__ rs_x, const double* __restrict__ bary_x,
-                         const double* __restrict__ stat_x, const double* __restrict__ rs_p,
-                         const double* __restrict__ bary_p, const double* __restrict__ stat_p,
-                         const double* __restrict__ f, const double* __restrict__ pp,
-                         double* warm_f, double* warm_p, int* warm_valid, double* flow,
-                         double* fstat, const double* scal, int* plan_state, int iteration,
-                         double* flow_log, double conv_tol, double* part, unsigned* count) {
-    __shared__ double scratch[32];
-    __shared__ bool s_last;
-    if (plan_state && *((volatile int*)plan_state) != 0) return;
-    const double ex = stat_x[0], ep = stat_p[0];
-    const double worst = (ex > ep || ex != ex) ? ex : ep;
-    const bool flow_error = worst > 100.0 * tol;
-    double norm_acc = 0.0;
-    if (!flow_error) {
-        for (int i = blockIdx.x * FIN_BLOCK + threadIdx.x; i < n; i += gridDim.x * FIN_BLOCK) {
-            const double rcx = rs_x[i], rux = bary_x[(size_t)i * (d + 1)];
-            const double rcp = rs_p[i], rup = bary_p[(size_t)i * (d + 1)];
-            double sq = 0.0;
-            for (int k = 0; k < d; ++k) {
-                const double x = X[(size_t)i * d + k];
-                const double ty = rux * bary_x[(size_t)i * (d + 1) + 1 + k];
-                const double px = rup * bary_p[(size_t)i * (d + 1) + 1 + k];
-                const double grad = 2.0 * (rcx * x - ty) - 2.0 * (rcp * x - px);
-                flow[(size_t)i * d + k] = -grad;
-                sq += grad * grad;
-            }
-            norm_acc += sqrt(sq);
-            if (warm_f) {
-                warm_f[i] = f[i];
-                warm_p[i] = pp[i];
-            }
-        }
-    }
-    const double blk = block_sum<FIN_BLOCK>(norm_acc, scratch);
-    if (threadIdx.x == 0) {
-        part[blockIdx.x] = blk;
-        __threadfence();
-        s_last = atomicAdd(count, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    double a = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += FIN_BLOCK) a += __ldcg(part + b);
-    const double total = block_sum<FIN_BLOCK>(a, scratch);
-    if (threadIdx.x == 0) {
-        *count = 0u;
-        const double mean_mag = total / n;
-        fstat[0] = worst;
-        fstat[1] = (stat_x[2] != 0.0 && stat_p[2] != 0.0) ? 1.0 : 0.0;
-        fstat[2] = flow_error ? 1.0 : 0.0;
-        fstat[3] = flow_error ? NAN : mean_mag;
-        fstat[4] = scal[SC_OMEGA];
-        fstat[5] = stat_x[1];
-        fstat[6] = stat_p[1];
-        fstat[7] = 0.0;
-        if (!flow_error && warm_valid) {
-            warm_valid[0] = 1;
-            warm_valid[1] = 1;
-        }
-        if (plan_state) {
-            if (flow_error) {
-                plan_state[FCB_STATE_STOP] = 2;
-                plan_state[FCB_STATE_STAGE] = 2;
-                plan_state[FCB_STATE_ITER] = iteration;
-                plan_state[FCB_STATE_INDEX] = -1;
-            } else {
-                double* lg = flow_log + 4 * (size_t)iteration;
-                lg[0] = mean_mag;
-                lg[1] = stat_x[1];
-                lg[2] = stat_p[1];
-                lg[3] = worst;
-                plan_state[FCB_STATE_FLOWS] = iteration + 1;
-                if (mean_mag < conv_tol) plan_state[FCB_STATE_STOP] = 1;
-            }
-        }
-    }
-}
-
 __global__ void divergence_combine_kernel(const double* costs, double* out) {
     if (threadIdx.x == 0) {
         out[1] = costs[0];
@@ -1082,26 +1222,45 @@ __global__ void copy_scal_kernel(const double* src, double* dst, const double* c
     }
 }
 
+// Workspace of sinkhorn_flow: scalars, both solves' outputs and their
+// OT layouts (both live at once in the one-launch flow kernel).
 struct FlowWs {
     double* scal;
     double* scal_self;
-    void* omega_ws;
+    double* part;
+    double* fin_part;
     double *f, *g, *rs_x, *stat_x, *bary_x;
     double *p, *rs_p, *stat_p, *bary_p;
-    double *f0, *p0;
-    double* fin_part;
-    unsigned* fin_count;
-    void* ot_ws;
-    size_t ot_bytes;
+    char* ws_a;
+    char* ws_b;
+    size_t bytes_a, bytes_b;
     size_t total;
 };
 
-static FlowWs flow_layout(int precision, int n, int m, int d, void* ws, size_t bytes) {
+template <typename Real, int D, int RPT>
+static int flow_grid_size(int* grid) {
+    static int cached = -1;
+    if (cached < 0) {
+        int per_sm = 0;
+        FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<Real, D, RPT>,
+                                                               OT_BLOCK, 0));
+        if (per_sm < 1) return fail(FCB_ECUDA, "flow_kernel cannot be resident");
+        int cap = 2;
+        if (const char* env = getenv("FCB_OT_CTAS_PER_SM")) cap = std::max(1, atoi(env));
+        cached = std::min(per_sm, cap) * sm_count();
+    }
+    *grid = cached;
+    return FCB_OK;
+}
+
+template <typename Real>
+static FlowWs flow_layout_t(int n, int m, int d, int rpt, int grid, void* ws, size_t bytes) {
     Arena ar(ws, bytes);
     FlowWs L{};
     L.scal = ar.take<double>(16);
     L.scal_self = ar.take<double>(16);
-    L.omega_ws = ar.take<char>(omega_ws_bytes(n, m));
+    L.part = ar.take<double>((size_t)grid * 8);
+    L.fin_part = ar.take<double>(grid);
     L.f = ar.take<double>(n);
     L.g = ar.take<double>(m);
     L.rs_x = ar.take<double>(n);
@@ -1111,52 +1270,125 @@ static FlowWs flow_layout(int precision, int n, int m, int d, void* ws, size_t b
     L.rs_p = ar.take<double>(n);
     L.stat_p = ar.take<double>(4);
     L.bary_p = ar.take<double>((size_t)n * (d + 1));
-    L.f0 = ar.take<double>(n);
-    L.p0 = ar.take<double>(n);
-    L.fin_part = ar.take<double>(FIN_GRID);
-    L.fin_count = ar.take<unsigned>(4);
-    L.ot_bytes = std::max(ot_ws_bytes(FCB_OT_ASYM, precision, n, m, d),
-                          ot_ws_bytes(FCB_OT_SYM, precision, n, n, d));
-    L.ot_ws = ar.take<char>(L.ot_bytes);
+    OtLayout<Real> la, lb;
+    ot_layout<Real>(la, FCB_OT_ASYM, n, m, d, rpt, grid, nullptr, 0);
+    ot_layout<Real>(lb, FCB_OT_SYM, n, n, d, rpt, grid, nullptr, 0);
+    L.bytes_a = la.bytes;
+    L.bytes_b = lb.bytes;
+    L.ws_a = ar.take<char>(la.bytes);
+    L.ws_b = ar.take<char>(lb.bytes);
     L.total = ar.off + 256;
     return L;
 }
 
+template <typename Real, int RPT>
+static int flow_grid_any(int d, int* grid) {
+    if (d == 1) return flow_grid_size<Real, 1, RPT>(grid);
+    if (d == 2) return flow_grid_size<Real, 2, RPT>(grid);
+    return flow_grid_size<Real, 3, RPT>(grid);
+}
+
 size_t sinkhorn_flow_ws_bytes(int precision, int n, int m, int d) {
-    return flow_layout(precision, n, m, d, nullptr, 0).total;
+    if (d < 1 || d > 3) return 0;
+    int grid = 0;
+    if (precision == FCB_FP64) {
+        if (flow_grid_any<double, RPT_F64>(d, &grid)) grid = 2 * sm_count();
+        return flow_layout_t<double>(n, m, d, RPT_F64, grid, nullptr, 0).total;
+    }
+    if (flow_grid_any<float, RPT_F32>(d, &grid)) grid = 2 * sm_count();
+    return flow_layout_t<float>(n, m, d, RPT_F32, grid, nullptr, 0).total;
 }
 
 static double unit_for(int precision) { return precision == FCB_FP64 ? 1.0 : kLog2e; }
+
+template <typename Real, int D, int RPT>
+static int flow_launch(const double* X, int n, const double* Y, int m, double omega_fixed,
+                       int max_iters, double tol, double* warm_f, double* warm_p, int* warm_valid,
+                       double* flow, double* fstat, int* plan_state, int iteration,
+                       double* flow_log, double conv_tol, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+    int grid = 0;
+    int rc = flow_grid_size<Real, D, RPT>(&grid);
+    if (rc) return rc;
+    FlowWs L = flow_layout_t<Real>(n, m, D, RPT, grid, ws, ws_bytes);
+    if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "sinkhorn_flow workspace too small");
+    FlowArgs<Real> fa{};
+    OtLayout<Real> la, lb;
+    ot_layout<Real>(la, FCB_OT_ASYM, n, m, D, RPT, grid, L.ws_a, L.bytes_a);
+    ot_layout<Real>(lb, FCB_OT_SYM, n, n, D, RPT, grid, L.ws_b, L.bytes_b);
+    fa.a = la.a;
+    fa.b = lb.a;
+    const double loga = -log((double)n), logb = -log((double)m);
+    for (OtArgs<Real>* o : {&fa.a, &fa.b}) {
+        o->X = X;
+        o->max_iters = max_iters;
+        o->tol = tol;
+        o->loga = loga;
+        o->bary = nullptr;
+        o->gate = nullptr;
+        o->scal = nullptr;
+        o->f0 = nullptr;
+    }
+    fa.a.Y = Y;
+    fa.a.logb = logb;
+    fa.a.f_out = L.f;
+    fa.a.g_out = L.g;
+    fa.a.rs_out = L.rs_x;
+    fa.a.stat = L.stat_x;
+    fa.a.bary = L.bary_x;
+    fa.b.Y = nullptr;
+    fa.b.logb = 0.0;
+    fa.b.f_out = L.p;
+    fa.b.g_out = nullptr;
+    fa.b.rs_out = L.rs_p;
+    fa.b.stat = L.stat_p;
+    fa.b.bary = L.bary_p;
+    fa.b.bar = fa.a.bar;  // one barrier and work counter for the whole flow
+    fa.omega_fixed = omega_fixed;
+    fa.part = L.part;
+    fa.scal = L.scal;
+    fa.scal_self = L.scal_self;
+    fa.warm_f = warm_f;
+    fa.warm_p = warm_p;
+    fa.warm_valid = (warm_f && warm_p) ? warm_valid : nullptr;
+    fa.flow = flow;
+    fa.fstat = fstat;
+    fa.plan_state = plan_state;
+    fa.iteration = iteration;
+    fa.flow_log = flow_log;
+    fa.conv_tol = conv_tol;
+    fa.fin_part = L.fin_part;
+    FCB_CUDA(cudaMemsetAsync(fa.a.bar, 0, sizeof(GridBarrier), st));
+    void* args[] = {&fa};
+    FCB_CUDA(cudaLaunchCooperativeKernel((const void*)flow_kernel<Real, D, RPT>, dim3(grid),
+                                         dim3(OT_BLOCK), args, 0, st));
+    FCB_LAUNCHED("flow_kernel");
+    return FCB_OK;
+}
 
 int sinkhorn_flow(int precision, const double* X, int n, const double* Y, int m, int d,
                   double omega_fixed, int max_iters, double tol, double* warm_f, double* warm_p,
                   int* warm_valid, double* flow, double* fstat, int* plan_state, int iteration,
                   double* flow_log, double conv_tol, void* ws, size_t ws_bytes,
                   cudaStream_t st) {
-    FlowWs L = flow_layout(precision, n, m, d, ws, ws_bytes);
-    if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "sinkhorn_flow workspace too small");
-    // omega, both centrings (the self term shares omega but is centred on X)
-    // and the warm-start selection in two launches
-    const bool warm = warm_f && warm_valid;
-    const double* f0 = warm ? L.f0 : nullptr;
-    const double* p0 = warm ? L.p0 : nullptr;
-    int rc = omega_prep(FCB_OT_ASYM, X, n, Y, m, d, omega_fixed, unit_for(precision), L.scal,
-                        L.scal_self, warm_f, warm_p, warm_valid, warm ? L.f0 : nullptr,
-                        warm ? L.p0 : nullptr, L.fin_count, L.omega_ws, omega_ws_bytes(n, m), st);
-    if (rc) return rc;
-    rc = ot_solve(FCB_OT_ASYM, precision, X, n, Y, m, d, L.scal, max_iters, tol, f0, L.f, L.g,
-                  L.rs_x, L.stat_x, L.bary_x, plan_state, L.ot_ws, L.ot_bytes, st);
-    if (rc) return rc;
-    rc = ot_solve(FCB_OT_SYM, precision, X, n, nullptr, 0, d, L.scal_self, max_iters, tol, p0, L.p,
-                  nullptr, L.rs_p, L.stat_p, L.bary_p, plan_state, L.ot_ws, L.ot_bytes, st);
-    if (rc) return rc;
-    const int fin_grid = std::max(1, std::min(FIN_GRID, (n + 2 * FIN_BLOCK - 1) / (2 * FIN_BLOCK)));
-    flow_finalize_kernel<<<fin_grid, FIN_BLOCK, 0, st>>>(
-        X, n, d, tol, L.rs_x, L.bary_x, L.stat_x, L.rs_p, L.bary_p, L.stat_p, L.f, L.p, warm_f,
-        warm_p, warm_valid, flow, fstat, L.scal, plan_state, iteration, flow_log, conv_tol,
-        L.fin_part, L.fin_count);
-    FCB_LAUNCHED("flow_finalize_kernel");
-    return FCB_OK;
+    if (n < 1 || m < 1) return fail(FCB_EINPUT, "empty point set");
+    if (max_iters < 1) return fail(FCB_EINPUT, "max_iters must be >= 1");
+#define FCB_FLOW_CASE(DD)                                                                        \
+    if (d == DD) {                                                                               \
+        if (precision == FCB_FP64)                                                               \
+            return flow_launch<double, DD, RPT_F64>(X, n, Y, m, omega_fixed, max_iters, tol,     \
+                                                    warm_f, warm_p, warm_valid, flow, fstat,     \
+                                                    plan_state, iteration, flow_log, conv_tol,   \
+                                                    ws, ws_bytes, st);                           \
+        return flow_launch<float, DD, RPT_F32>(X, n, Y, m, omega_fixed, max_iters, tol, warm_f,  \
+                                               warm_p, warm_valid, flow, fstat, plan_state,      \
+                                               iteration, flow_log, conv_tol, ws, ws_bytes, st); \
+    }
+    FCB_FLOW_CASE(1)
+    FCB_FLOW_CASE(2)
+    FCB_FLOW_CASE(3)
+#undef FCB_FLOW_CASE
+    return fail(FCB_ENOTSUP, "point dimension must be 1, 2 or 3");
 }
 
 struct DivWs {
