@@ -1288,8 +1288,19 @@ static int flow_grid_any(int d, int* grid) {
     return flow_grid_size<Real, 3, RPT>(grid);
 }
 
+// flow_resident.cu: the one-launch flow with the point sets in shared memory
+bool sinkhorn_flow_resident_fits(int n, int m, int d);
+size_t sinkhorn_flow_resident_ws_bytes(int n, int m, int d);
+int sinkhorn_flow_resident(const double* X, int n, const double* Y, int m, int d,
+                           double omega_fixed, int max_iters, double tol, double* warm_f,
+                           double* warm_p, int* warm_valid, double* flow, double* fstat,
+                           int* plan_state, int iteration, double* flow_log, double conv_tol,
+                           void* ws, size_t ws_bytes, cudaStream_t st);
+
 size_t sinkhorn_flow_ws_bytes(int precision, int n, int m, int d) {
     if (d < 1 || d > 3) return 0;
+    if (precision != FCB_FP64 && sinkhorn_flow_resident_fits(n, m, d))
+        return sinkhorn_flow_resident_ws_bytes(n, m, d);
     int grid = 0;
     if (precision == FCB_FP64) {
         if (flow_grid_any<double, RPT_F64>(d, &grid)) grid = 2 * sm_count();
@@ -1373,6 +1384,10 @@ int sinkhorn_flow(int precision, const double* X, int n, const double* Y, int m,
                   cudaStream_t st) {
     if (n < 1 || m < 1) return fail(FCB_EINPUT, "empty point set");
     if (max_iters < 1) return fail(FCB_EINPUT, "max_iters must be >= 1");
+    if (precision != FCB_FP64 && sinkhorn_flow_resident_fits(n, m, d))
+        return sinkhorn_flow_resident(X, n, Y, m, d, omega_fixed, max_iters, tol, warm_f, warm_p,
+                                      warm_valid, flow, fstat, plan_state, iteration, flow_log,
+                                      conv_tol, ws, ws_bytes, st);
 #define FCB_FLOW_CASE(DD)                                                                        \
     if (d == DD) {                                                                               \
         if (precision == FCB_FP64)                                                               \
