@@ -41,6 +41,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
+#include <atomic>
 
 namespace fcb {
 
@@ -116,6 +117,7 @@ struct RsArgs {
     int nqpA, nqpB, nqpS;     // padded quads of the three column sets
     int ldA, ldB;             // floats per array of smem regions A and B
     int cache_off, cache_rows;  // own-row cache (floats offset, rows; 0: none)
+    unsigned launch_id;         // grid groups: epoch of this launch (barrier reset)
 };
 
 // Shared-memory column set: D coordinate arrays and the folded potential,
@@ -654,6 +656,16 @@ __global__ void __launch_bounds__(RS_BLOCK, 1) rs_flow_kernel(RsArgs A) {
     double* flow_log = A.flow_log ? A.flow_log + (size_t)b * A.log_stride : nullptr;
     const int tid = threadIdx.x;
     RS_MARK(0);
+    // grid groups: CTA 0 resets the barrier and done counters for this launch
+    // and publishes the launch epoch; the others wait for it before their
+    // first arrival (no host-side memset between launches)
+    if (GRID && blockIdx.x == 0 && tid == 0) {
+        A.bar->count = 0u;
+        *A.done = 0u;
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&A.bar->work), "r"(A.launch_id)
+                     : "memory");
+    }
 
     // ---- statistics (every CTA, fixed order) -> omega, centres -------------
     {
@@ -750,6 +762,9 @@ __global__ void __launch_bounds__(RS_BLOCK, 1) rs_flow_kernel(RsArgs A) {
         errslot[0] = 0ull;
         errslot[1] = 0ull;
         errslot[2] = 0ull;
+    }
+    if (GRID && blockIdx.x != 0 && tid == 0) {
+        while (ld_acquire_u32(&A.bar->work) != A.launch_id) __nanosleep(32);
     }
     __syncthreads();
     RS_MARK(1);
@@ -1219,8 +1234,8 @@ int sinkhorn_flow_resident(const double* X, int n, const double* Y, int m, int d
     if (getenv("FCB_RS_VERBOSE"))
         fprintf(stderr, "rs_flow: n=%d m=%d d=%d G=%d plan A=%d/%d B=%d/%d S=%d/%d smem=%zu\n", n, m,
                 d, G, 1 << sh.A.cg, sh.A.nr, 1 << sh.B.cg, sh.B.nr, 1 << sh.S.cg, sh.S.nr, sh.smem);
-    // the barrier and done counters restart at zero every launch
-    FCB_CUDA(cudaMemsetAsync(L.bar, 0, (size_t)((char*)(L.done + 32) - (char*)L.bar), st));
+    static std::atomic<unsigned> launches{0};
+    a.launch_id = 0x9e3779b9u * (launches.fetch_add(1u) + 1u) | 1u;
     switch (d) {
         case 1: return rs_launch<1, true>(a, G, sh.smem, st);
         case 2: return rs_launch<2, true>(a, G, sh.smem, st);

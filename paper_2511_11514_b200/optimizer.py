@@ -309,22 +309,29 @@ def plan_detailed(
         _lib.check(rc, name)
 
     ring = [torch.zeros(8, dtype=torch.int32, pin_memory=True) for _ in range(poll_lag + 2)]
+    # status snapshots every `poll_every` iterations: after a stop, the queued
+    # kernels are gated by the device status word and exit at once
+    poll_every = 8
+    e_prev = None
     for it in range(maxit):
         cur = it & 1
-        e0 = torch.cuda.Event(enable_timing=True)
-        e0.record()
+        if e_prev is None:
+            e_prev = torch.cuda.Event(enable_timing=True)
+            e_prev.record()
+        e0 = e_prev  # the previous iteration's end event
         call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0),
              _dev.ptr(Ubuf[cur]), T, float(disc.dt), _dev.ptr(Sbuf[cur]), d, _dev.ptr(P),
              _dev.ptr(X), None, state_ptr, it, 1, _dev.ptr(roll_ws), stream)
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
+        e2 = e1
         if want_metric and it % cfg.metric_interval == 0:
             call("fcb_sinkhorn_divergence", mprec, _dev.ptr(X), T, _dev.ptr(Ymd), Mm, d,
                  _omega_arg(cfg.sinkhorn.omega), cfg.sinkhorn.max_iters, cfg.sinkhorn.tol,
                  _dev.ptr(metric_vals[it // cfg.metric_interval]), state_ptr,
                  _dev.ptr(met_ws), met_ws.numel(), stream)
-        e2 = torch.cuda.Event(enable_timing=True)
-        e2.record()
+            e2 = torch.cuda.Event(enable_timing=True)
+            e2.record()
         if cfg.method == "sinkhorn":
             call("fcb_sinkhorn_flow", prec, _dev.ptr(X), T, _dev.ptr(Yd), M, d, omega_fixed,
                  scfg.max_iters, scfg.tol, _dev.ptr(warm_f), _dev.ptr(warm_p),
@@ -347,10 +354,13 @@ def plan_detailed(
              _dev.ptr(upd_ws), upd_ws.numel(), stream)
         e4 = torch.cuda.Event(enable_timing=True)
         e4.record()
+        e_prev = e4
         marks.append((e0, e1, e2, e3, e4))
+        if (it + 1) % poll_every != 0 and it + 1 < maxit:
+            continue
         # asynchronous status snapshot; the host stays at most poll_lag
-        # iterations ahead of the device and stops queueing after a stop
-        snap = ring[it % len(ring)]
+        # snapshots ahead of the device and stops queueing after a stop
+        snap = ring[(it // poll_every) % len(ring)]
         snap.copy_(state, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()

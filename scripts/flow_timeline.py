@@ -47,3 +47,29 @@ for it in range(len(log)):
           f" ({(rel[a1 - 1] - rel[1]) / max(ncross, 1):5.1f}/it) | sym {rel[s1 - 1] - rel[a1 - 1]:5.1f}"
           f" | end {rel[-1] - rel[s1 - 1]:5.1f} | gap before {gap:6.1f}")
     pos += 2 * nbar
+
+# per-phase critical path of the asymmetric iterations (release-to-release)
+pos = 0
+acc = np.zeros(3)
+cnt = 0
+sym = np.zeros(2)
+scnt = 0
+for it in range(len(log)):
+    ncross, nself = int(log[it, 1]), int(log[it, 2])
+    nbar = 2 + 3 * ncross + 2 * nself + 2
+    st = t[pos:pos + 2 * nbar]
+    if len(st) < 2 * nbar:
+        break
+    rel = st[1::2]
+    for k in range(ncross):
+        b = 2 + 3 * k
+        acc += [rel[b] - rel[b - 1], rel[b + 1] - rel[b], rel[b + 2] - rel[b + 1]]
+        cnt += 1
+    for k in range(nself):
+        b = 2 + 3 * ncross + 2 * k
+        sym += [rel[b] - rel[b - 1], rel[b + 1] - rel[b]]
+        scnt += 1
+    pos += 2 * nbar
+print(f"asym per-iteration critical path (us): sweepA {acc[0]/cnt:.2f} sweepB(+mergeA) {acc[1]/cnt:.2f} "
+      f"mergeB+err {acc[2]/cnt:.2f}  (n={cnt})")
+print(f"sym per-iteration (us): sweep {sym[0]/scnt:.2f} merge {sym[1]/scnt:.2f} (n={scnt})")

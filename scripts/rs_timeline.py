@@ -48,6 +48,10 @@ for key in sorted(stat, key=lambda k: -sum(stat[k])):
     v = stat[key]
     print(f"{names.get(key[0], key[0]):>9} -> {names.get(key[1], key[1]):<9} n={len(v):5d} "
           f"mean {np.mean(v):7.2f} us  total {np.sum(v):9.1f} us")
+gaps = [t[i + 1] - t[i] for i in range(len(tags) - 1) if tags[i] == 15 and tags[i + 1] == 0]
+if gaps:
+    print(f"between flow launches (CTA 0 end -> next start): mean {np.mean(gaps):.1f} us, "
+          f"median {np.median(gaps):.1f} us, n={len(gaps)}")
 ka = run.flow_log[:, 1].sum()
 ks = run.flow_log[:, 2].sum()
 print(f"inner iterations: asym {ka:.0f} self {ks:.0f}; flows {len(run.flow_log)}")
