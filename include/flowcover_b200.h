@@ -239,6 +239,32 @@ FCB_API int fcb_plan_update(int model, int ns, int m, const double* model_params
                     int iteration, int mode, double* ws, size_t ws_bytes, fcb_stream_t stream);
 FCB_API size_t fcb_plan_update_workspace_bytes(int ns, int m, int T);
 
+/* The coverage loop of optimizer.py:221-269 for iterations it0..maxit-1 in ONE
+ * persistent launch (rollout -> Sinkhorn flow -> LQR affine phase -> control
+ * update, device-side stop tests), for the built-in linear models (single /
+ * double integrator) with the fp32 resident flow (point sets on chip) and no
+ * in-loop metric.  Replaces the per-iteration fcb_rollout / fcb_sinkhorn_flow /
+ * fcb_plan_update sequence of the planner (optimizer.py:221-269); results
+ * follow the same semantics (warm state, flow_log rows, lqr_costs, plan_state
+ * stop codes).  U0/U1 and S0/S1: controls and states of even / odd iterations
+ * (iteration it reads U_{it&1}, writes U_{(it+1)&1}).  upd_ws: the
+ * fcb_plan_update workspace after a mode-0 call (stored Riccati phase).
+ * batch > 1: independent problems of the same shape, one CTA each (inputs
+ * stacked per problem: s0, U, S, X, flow, Y, warm state, fstat [8], plan_state
+ * [8], flow_log [4*maxit], lqr_costs [maxit], phase_ns [3]); batch 1 spreads
+ * the problem over every SM.  Returns FCB_ENOTSUP when the shape/model is not
+ * covered (the caller keeps the per-iteration path). */
+FCB_API size_t fcb_plan_fused_workspace_bytes(int batch, int T, int M, int d, int m);
+FCB_API int fcb_plan_fused(int model, int ns, int m, const double* model_params, const double* s0,
+                   double* U0, double* U1, double* S0, double* S1, int T, double dt, int d,
+                   const double* P, double* X, double* flow, const double* Q, const double* R,
+                   double eta, const double* clamp, const double* Y, int M, double omega_fixed,
+                   int max_iters, double tol, double conv_tol, double* warm_f, double* warm_p,
+                   int* warm_valid, double* fstat, int* plan_state, double* flow_log,
+                   double* lqr_costs, unsigned long long* phase_ns, int it0, int maxit,
+                   int batch, const void* upd_ws, void* ws, size_t ws_bytes,
+                   fcb_stream_t stream);
+
 /* ---- measurement helpers ------------------------------------------------- */
 
 /* MUFU.EX2 / FFMA throughput probe used by bench.py for the roofline

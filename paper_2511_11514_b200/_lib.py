@@ -96,6 +96,12 @@ SIGNATURES: dict[str, tuple] = {
         [_I, _I, _I, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P, _I, _I, _P, _Z,
          _P],
     ),
+    "fcb_plan_fused_workspace_bytes": (_Z, [_I, _I, _I, _I, _I]),
+    "fcb_plan_fused": (
+        _I,
+        [_I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _P, _D, _P, _P, _I, _D,
+         _I, _D, _D, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _Z, _P],
+    ),
     "fcb_peak_probe": (_I, [_I, _I, _P, _P]),
     "fcb_debug_timeline": (_I, [_P, _I]),
 }

@@ -97,6 +97,16 @@ int plan_update(int model, int ns, int m, const double* prm, const double* S, co
                 int* plan_state, int iteration, int mode, double* ws, size_t ws_bytes,
                 cudaStream_t st);
 
+size_t plan_fused_ws_bytes(int batch, int T, int M, int d, int mc);
+int plan_fused(int model, int ns, int m, const double* prm, const double* s0, double* U0,
+               double* U1, double* S0, double* S1, int T, double dt, int d, const double* P,
+               double* X, double* flow, const double* Q, const double* R, double eta,
+               const double* clamp, const double* Y, int M, double omega_fixed, int max_iters,
+               double tol, double conv_tol, double* warm_f, double* warm_p, int* warm_valid,
+               double* fstat, int* plan_state, double* flow_log, double* lqr_costs,
+               unsigned long long* phase_ns, int it0, int maxit, int batch, const void* upd_ws,
+               void* ws, size_t ws_bytes, cudaStream_t st);
+
 // ---- peak probe: MUFU.EX2 and FFMA throughput -----------------------------
 constexpr int PROBE_BLOCK = 256;
 
@@ -295,6 +305,27 @@ int fcb_lqr_solve(int ns, int m, int T, double dt, const double* A, const double
                   fcb_stream_t stream) {
     if (!(dt > 0.0)) return fail(FCB_EINPUT, "dt must be positive");
     return lqr_solve(ns, m, T, dt, A, B, Q, R, a, v, z, K, dff, scal, status, ws, CS(stream));
+}
+
+size_t fcb_plan_fused_workspace_bytes(int batch, int T, int M, int d, int m) {
+    return plan_fused_ws_bytes(batch, T, M, d, m);
+}
+
+int fcb_plan_fused(int model, int ns, int m, const double* model_params, const double* s0,
+                   double* U0, double* U1, double* S0, double* S1, int T, double dt, int d,
+                   const double* P, double* X, double* flow, const double* Q, const double* R,
+                   double eta, const double* clamp, const double* Y, int M, double omega_fixed,
+                   int max_iters, double tol, double conv_tol, double* warm_f, double* warm_p,
+                   int* warm_valid, double* fstat, int* plan_state, double* flow_log,
+                   double* lqr_costs, unsigned long long* phase_ns, int it0, int maxit,
+                   int batch, const void* upd_ws, void* ws, size_t ws_bytes,
+                   fcb_stream_t stream) {
+    if (!(dt > 0.0)) return fail(FCB_EINPUT, "dt must be positive");
+    if (T < 1 || M < 1 || batch < 1) return fail(FCB_EINPUT, "empty problem");
+    return plan_fused(model, ns, m, model_params, s0, U0, U1, S0, S1, T, dt, d, P, X, flow, Q, R,
+                      eta, clamp, Y, M, omega_fixed, max_iters, tol, conv_tol, warm_f, warm_p,
+                      warm_valid, fstat, plan_state, flow_log, lqr_costs, phase_ns, it0, maxit,
+                      batch, upd_ws, ws, ws_bytes, CS(stream));
 }
 
 size_t fcb_plan_update_workspace_bytes(int ns, int m, int T) {

@@ -816,6 +816,169 @@ int plan_update(int model, int ns, int m, const double* prm, const double* S, co
     return FCB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// the fused planner loop (plan_fused.cuh)
+// ---------------------------------------------------------------------------
+}  // namespace fcb
+#include "plan_fused.cuh"
+namespace fcb {
+
+struct PfWs {
+    RsWs rs;
+    double* agg;
+    double* part;
+    int* ipart;
+    double* dff;
+    size_t total;
+};
+
+static PfWs pf_layout(int batch, int n, int m, int d, int mc, int group, void* ws, size_t bytes) {
+    PfWs L{};
+    L.rs = rs_layout(batch, n, m, d, group, ws, bytes);
+    Arena ar(ws ? (char*)ws + L.rs.total : nullptr, ws ? (bytes > L.rs.total ? bytes - L.rs.total : 0) : 0);
+    L.agg = ar.take<double>((size_t)2 * PF_CARRY * (6 * 6 + 6));
+    L.part = ar.take<double>(PF_CARRY);
+    L.ipart = ar.take<int>(PF_CARRY);
+    L.dff = ar.take<double>((size_t)batch * n * mc);
+    L.total = L.rs.total + ar.off + 256;
+    return L;
+}
+
+size_t plan_fused_ws_bytes(int batch, int T, int M, int d, int mc) {
+    const int G = batch > 1 ? 1 : sm_count();
+    return pf_layout(batch, T, M, d, mc, G, nullptr, 0).total;
+}
+
+template <class Mdl, int D, bool GRID>
+static int pf_launch(const RsArgs& a, const PlanFusedArgs<Mdl::N, Mdl::M>& pf, int grid,
+                     size_t smem, cudaStream_t st) {
+    auto kern = rs_plan_kernel<D, GRID, Mdl>;
+    static size_t attr = 0;
+    if (attr < smem) {
+        FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+    }
+    RsArgs ac = a;
+    PlanFusedArgs<Mdl::N, Mdl::M> pc = pf;
+    if (GRID) {
+        void* args[] = {&ac, &pc};
+        FCB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(RS_BLOCK), args,
+                                             smem, st));
+    } else {
+        kern<<<grid, RS_BLOCK, smem, st>>>(ac, pc);
+    }
+    FCB_LAUNCHED("rs_plan_kernel");
+    return FCB_OK;
+}
+
+template <class Mdl>
+static int plan_fused_t(const double* prm, const double* s0, double* U0, double* U1, double* S0,
+                        double* S1, int T, double dt, int d, const double* P, double* X,
+                        double* flow, const double* Q, const double* R, double eta,
+                        const double* clamp, const double* Y, int M, double omega_fixed,
+                        int max_iters, double tol, double conv_tol, double* warm_f,
+                        double* warm_p, int* warm_valid, double* fstat, int* plan_state,
+                        double* flow_log, double* lqr_costs, unsigned long long* phase_ns,
+                        int it0, int maxit, int batch, const void* upd_ws, void* ws,
+                        size_t ws_bytes, cudaStream_t st) {
+    constexpr int N = Mdl::N, MC = Mdl::M;
+    if constexpr (!Mdl::LINEAR || N > 4) {
+        return fail(FCB_ENOTSUP, "the fused planner needs a linear model with at most 4 states");
+    } else {
+        const bool grid_mode = batch <= 1;
+        const int G = grid_mode ? sm_count() : 1;
+        if (G > PF_CARRY) return fail(FCB_ENOTSUP, "too many SMs for the fused planner");
+        const RsShape sh = rs_shape(T, M, d, G, grid_mode);
+        if (!sh.ok) return fail(FCB_ENOTSUP, "point sets do not fit in shared memory");
+        const size_t smem = std::max(sh.smem, pf_smem_bytes<N>());
+        if (smem + RS_STATIC_SMEM > (size_t)rs_smem_limit())
+            return fail(FCB_ENOTSUP, "fused planner shared memory");
+        PfWs L = pf_layout(batch, T, M, d, MC, G, ws, ws_bytes);
+        if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "plan_fused workspace too small");
+        LqrWs W = lqr_layout(N, MC, T, const_cast<void*>(upd_ws));
+        RsArgs a{};
+        a.X = X;
+        a.Y = Y;
+        a.n = T;
+        a.m = M;
+        a.omega_fixed = omega_fixed;
+        a.max_iters = max_iters;
+        a.tol = tol;
+        a.conv_tol = conv_tol;
+        a.warm_f = warm_f;
+        a.warm_p = warm_p;
+        a.warm_valid = (warm_f && warm_p) ? warm_valid : nullptr;
+        a.flow = flow;
+        a.fstat = fstat;
+        a.plan_state = plan_state;
+        a.iteration = it0;
+        a.flow_log = flow_log;
+        a.log_stride = 4LL * maxit;
+        rs_fill(a, L.rs, sh);
+        a.launch_id = next_launch_epoch();
+        PlanFusedArgs<N, MC> pf{};
+        pf.T = T;
+        pf.d = d;
+        pf.it0 = it0;
+        pf.maxit = maxit;
+        pf.dt = dt;
+        pf.eta = eta;
+        pf.s0 = s0;
+        pf.prm = prm;
+        pf.P = P;
+        pf.Q = Q;
+        pf.R = R;
+        pf.clamp = clamp;
+        pf.K = W.K;
+        pf.Lg = W.Lg;
+        pf.Acl = W.Acl;
+        pf.Gm = W.Gm;
+        pf.dff = L.dff;
+        pf.U0 = U0;
+        pf.U1 = U1;
+        pf.S0 = S0;
+        pf.S1 = S1;
+        pf.lqr_costs = lqr_costs;
+        pf.phase_ns = phase_ns;
+        pf.agg = L.agg;
+        pf.part = L.part;
+        pf.ipart = L.ipart;
+        const int grid = grid_mode ? G : batch;
+        // the built-in linear models cover a planar workspace
+        if (d != 2) return fail(FCB_ENOTSUP, "the fused planner covers planar workspaces");
+        return grid_mode ? pf_launch<Mdl, 2, true>(a, pf, grid, smem, st)
+                         : pf_launch<Mdl, 2, false>(a, pf, grid, smem, st);
+    }
+}
+
+int plan_fused(int model, int ns, int m, const double* prm, const double* s0, double* U0,
+               double* U1, double* S0, double* S1, int T, double dt, int d, const double* P,
+               double* X, double* flow, const double* Q, const double* R, double eta,
+               const double* clamp, const double* Y, int M, double omega_fixed, int max_iters,
+               double tol, double conv_tol, double* warm_f, double* warm_p, int* warm_valid,
+               double* fstat, int* plan_state, double* flow_log, double* lqr_costs,
+               unsigned long long* phase_ns, int it0, int maxit, int batch, const void* upd_ws,
+               void* ws, size_t ws_bytes, cudaStream_t st) {
+    int rc = check_dims(model, ns, m);
+    if (rc) return rc;
+    if (d < 1 || d > 3) return fail(FCB_ENOTSUP, "point dimension must be 1, 2 or 3");
+    if (it0 >= maxit) return FCB_OK;
+    switch (model) {
+        case FCB_MODEL_SINGLE_INTEGRATOR_2D:
+            return plan_fused_t<Model<FCB_MODEL_SINGLE_INTEGRATOR_2D>>(
+                prm, s0, U0, U1, S0, S1, T, dt, d, P, X, flow, Q, R, eta, clamp, Y, M, omega_fixed,
+                max_iters, tol, conv_tol, warm_f, warm_p, warm_valid, fstat, plan_state, flow_log,
+                lqr_costs, phase_ns, it0, maxit, batch, upd_ws, ws, ws_bytes, st);
+        case FCB_MODEL_DOUBLE_INTEGRATOR_2D:
+            return plan_fused_t<Model<FCB_MODEL_DOUBLE_INTEGRATOR_2D>>(
+                prm, s0, U0, U1, S0, S1, T, dt, d, P, X, flow, Q, R, eta, clamp, Y, M, omega_fixed,
+                max_iters, tol, conv_tol, warm_f, warm_p, warm_valid, fstat, plan_state, flow_log,
+                lqr_costs, phase_ns, it0, maxit, batch, upd_ws, ws, ws_bytes, st);
+        default:
+            return fail(FCB_ENOTSUP, "the fused planner supports the built-in linear models");
+    }
+}
+
 }  // namespace fcb
 
 // Debug: per-block stamps of the last one-launch scan (FCB_SCAN_TL builds).

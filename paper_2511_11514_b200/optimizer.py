@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import collections
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -313,8 +314,34 @@ def plan_detailed(
     # kernels are gated by the device status word and exit at once
     poll_every = 8
     e_prev = None
+    # linear models with the on-chip flow: iterations 1.. run as one
+    # persistent launch (fcb_plan_fused) after iteration 0 has stored the
+    # Riccati phase; anything it does not cover stays on the per-iteration path
+    fused_ok = (os.environ.get("FCB_FUSED", "1") != "0" and cfg.method == "sinkhorn"
+                and not want_metric and prec == _lib.FCB_FP32
+                and d == 2 and maxit > 1 and spec.model_id in (
+                    _lib.FCB_MODEL_SINGLE_INTEGRATOR_2D, _lib.FCB_MODEL_DOUBLE_INTEGRATOR_2D))
+    fused_ran = False
+    phase_ns = torch.zeros(3, dtype=torch.int64, device=dev) if fused_ok else None
     for it in range(maxit):
         cur = it & 1
+        if it == 1 and fused_ok:
+            fws = _dev.Workspace.get(
+                lib.fcb_plan_fused_workspace_bytes(1, T, M, d, m_c), "plan_fused")
+            rc = lib.fcb_plan_fused(
+                spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0), _dev.ptr(Ubuf[0]),
+                _dev.ptr(Ubuf[1]), _dev.ptr(Sbuf[0]), _dev.ptr(Sbuf[1]), T, float(disc.dt), d,
+                _dev.ptr(P), _dev.ptr(X), _dev.ptr(flow), _dev.ptr(Q), _dev.ptr(R),
+                float(cfg.eta), _dev.ptr(clamp_d), _dev.ptr(Yd), M, omega_fixed, scfg.max_iters,
+                scfg.tol, float(cfg.convergence_tol), _dev.ptr(warm_f), _dev.ptr(warm_p),
+                _dev.ptr(warm_valid), _dev.ptr(fstat), state_ptr, _dev.ptr(flow_log),
+                _dev.ptr(lqr_costs), _dev.ptr(phase_ns), 1, maxit, 1, _dev.ptr(upd_ws),
+                _dev.ptr(fws), fws.numel(), stream)
+            if rc == _lib.FCB_OK:
+                fused_ran = True
+                break
+            if rc != _lib.FCB_ENOTSUP:
+                _lib.check(rc, "fcb_plan_fused")
         if e_prev is None:
             e_prev = torch.cuda.Event(enable_timing=True)
             e_prev.record()
@@ -408,6 +435,11 @@ def plan_detailed(
         t_flow += e2.elapsed_time(e3) * 1e-3
         if k < updates:
             t_lqr += e3.elapsed_time(e4) * 1e-3
+    if fused_ran:  # device-side phase clocks of the persistent launch
+        pn = phase_ns.cpu().numpy().astype(np.float64) * 1e-9
+        t_roll += float(pn[0])
+        t_flow += float(pn[1])
+        t_lqr += float(pn[2])
 
     # final rollout on the last controls (optimizer.py:271-277)
     U_final = Ubuf[updates & 1]
