@@ -981,6 +981,24 @@ int plan_fused(int model, int ns, int m, const double* prm, const double* s0, do
 
 }  // namespace fcb
 
+// Debug (FCB_TIMELINE builds): CTA 0 phase stamps of the fused planner.
+extern "C" FCB_API int fcb_debug_plan_timeline(unsigned long long* host_out, int cap) {
+#ifdef FCB_TIMELINE
+    unsigned n = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&n, fcb::g_rs_tl_n, sizeof(unsigned));
+    const int k = (int)std::min<unsigned>(n, (unsigned)cap);
+    if (k) cudaMemcpyFromSymbol(host_out, fcb::g_rs_tl, k * sizeof(unsigned long long));
+    const unsigned zero = 0;
+    cudaMemcpyToSymbol(fcb::g_rs_tl_n, &zero, sizeof(unsigned));
+    return k;
+#else
+    (void)host_out;
+    (void)cap;
+    return -1;
+#endif
+}
+
 // Debug: per-block stamps of the last one-launch scan (FCB_SCAN_TL builds).
 extern "C" FCB_API int fcb_debug_scan_timeline(unsigned long long* host_out) {
 #ifdef FCB_SCAN_TL

@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
         double* Un = ((it & 1) ? pf.U0 : pf.U1) + oTM;
         double* S = ((it & 1) ? pf.S1 : pf.S0) + oTN;
         const unsigned long long t0 = pf_clock();
+        RS_MARK(50);
         // ---- rollout of U (dynamics.py:276-312) -> S, X -------------------
         if (tid == 0) s_first_bad = 0x7f7f7f7f;
         {
@@ -271,7 +272,9 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
             const AMap<N>* inc = pf_phase1<N, true>(T, chF, mapf, sm, GRID ? pf.agg : nullptr);
             if (GRID && first) rs_wait_epoch(A0);
             first = false;
+            RS_MARK(51);
             grp.sync();
+            RS_MARK(52);
             if (pending_finish && (!GRID || grp.rank == 0) && tid < 32) {
                 // the previous update's total cost (fixed order over CTAs)
                 const double tot = rs_ordered_sum(pf.part, grp.size);
@@ -283,7 +286,9 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
             pf_phase2<N, true, GRID>(T, chF, mapf, out, s0, sm, inc, GRID ? pf.agg : nullptr);
             __syncthreads();
             if (GRID && tid == 0) pf.ipart[grp.rank] = s_first_bad;
+            RS_MARK(53);
             grp.sync();
+            RS_MARK(54);
             const int fb = GRID ? pf_min_over(pf.ipart, grp.size, sm.ired) : s_first_bad;
             if (fb < 0x7f7f7f7f) {
                 if ((!GRID || grp.rank == 0) && tid == 0) roll_finish_body(fb, nullptr, plan_state, it);
@@ -291,6 +296,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
             }
         }
         const unsigned long long t1 = pf_clock();
+        RS_MARK(55);
         // ---- flow ------------------------------------------------------------
         {
             RsArgs A = A0;
@@ -298,13 +304,16 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
             rs_flow_body<D, GRID>(A, false);
         }
         const unsigned long long t2 = pf_clock();
+        RS_MARK(56);
         // ---- LQR affine phase (lqr.py:180-200 on the stored Riccati phase) ---
         if (tid == 0) {
             s_fail = -1;
         }
         const EtaMap<N, LiftedFlow<N>> emap{pf.Acl, pf.Q, pf.dt, T, lift};
         const AMap<N>* incE = pf_phase1<N, false>(T, chB, emap, sm, GRID ? pf.agg : nullptr);
+        RS_MARK(57);
         grp.sync();  // flow statistics and stop flags visible
+        RS_MARK(58);
         if (tid == 0) s_stop = *((volatile const int*)plan_state);
         __syncthreads();
         if (s_stop != 0) break;
@@ -316,7 +325,9 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
         if (GRID && tid == 0) pf.ipart[grp.rank] = -s_fail;  // min of -fail = -max fail
         const ZMap<N, M> zmap{pf.Acl, pf.Gm, dff, T};
         const AMap<N>* incZ = pf_phase1<N, true>(T, chF, zmap, sm, GRID ? pf.agg + (size_t)PF_CARRY * (N * N + N) : nullptr);
+        RS_MARK(59);
         grp.sync();
+        RS_MARK(60);
         const int fail_all = GRID ? -pf_min_over(pf.ipart, grp.size, sm.ired) : s_fail;
         if (fail_all >= 0) {
             if ((!GRID || grp.rank == 0) && tid == 0) {
@@ -341,6 +352,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
             lqr_finish_body(cs, &f, nullptr, lqr_costs, plan_state, it);
         }
         const unsigned long long t3 = pf_clock();
+        RS_MARK(61);
         tr += t1 - t0;
         tf += t2 - t1;
         tl += t3 - t2;
