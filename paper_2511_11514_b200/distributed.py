@@ -238,10 +238,11 @@ def plan_batch(problems: list, group=None) -> list:
     ...; results are gathered on every rank in problem order.  No collective
     touches the data path.
     """
-    from .optimizer import plan
+    from .optimizer import plan_batch as plan_local
 
     rank, world = _world(group)
-    mine = {i: plan(*problems[i]) for i in range(rank, len(problems), world)}
+    idx = list(range(rank, len(problems), world))
+    mine = dict(zip(idx, plan_local([problems[i] for i in idx])))
     if world == 1:
         return [mine[i] for i in range(len(problems))]
     gathered = [None] * world

@@ -498,3 +498,186 @@ def plan_detailed(
         pairs=_pair_count(cfg.method, log, T, M),
         launches=int(launches),
     )
+
+
+# ---------------------------------------------------------------------------
+# batched independent problems (BASELINE config 5)
+# ---------------------------------------------------------------------------
+def _batch_key(model: DynamicsModel, disc: Discretization, cfg: PlanConfig) -> tuple:
+    """Everything but the seed, the start state and the targets must agree."""
+    c = cfg
+    return (device_model(model).model_id, model.state_dim, model.control_dim,
+            model.workspace_dim, disc.num_steps, disc.dt, c.method, c.eta, c.max_iterations,
+            c.convergence_tol, c.control_clamp, c.init_scale, c.metric_interval, c.q_weight,
+            c.r_weight, c.sinkhorn, isinstance(c.initial_controls, str) and c.initial_controls)
+
+
+def plan_batch_detailed(problems: list) -> list[PlanRun]:
+    """Plan independent problems [(model, q, disc, cfg), ...] on this GPU.
+
+    Each result follows plan() of that problem (optimizer.py:171-304).  When
+    every problem is a built-in linear model with the same shapes and
+    configuration (seeds, start states and targets may differ), the Sinkhorn
+    method, no in-loop metric and point sets that fit on chip, the whole
+    batch runs as ONE launch of the fused planner with one problem per CTA
+    (fcb_plan_fused, batch > 1); otherwise the problems run one by one.  As in
+    a loop over plan(), the first failing problem (in order) raises its
+    PlanError.
+    """
+    if not problems:
+        return []
+    model, _q, disc, cfg = problems[0]
+    key = _batch_key(model, disc, cfg)
+    uniform = len(problems) > 1 and all(_batch_key(m, ds, c) == key for m, _, ds, c in problems)
+    spec = device_model(model)
+    T = disc.num_steps
+    d = model.workspace_dim
+    eligible = (uniform and cfg.method == "sinkhorn" and cfg.metric_interval == 0 and d == 2
+                and cfg.max_iterations >= 1 and os.environ.get("FCB_FUSED", "1") != "0"
+                and spec.model_id in (_lib.FCB_MODEL_SINGLE_INTEGRATOR_2D,
+                                      _lib.FCB_MODEL_DOUBLE_INTEGRATOR_2D))
+    targets = []
+    if eligible:
+        for m, q, ds, c in problems:
+            if ds.s0.shape != (m.state_dim,):
+                raise ValueError(f"s0 must have shape ({m.state_dim},), got {ds.s0.shape}")
+            tg = q if isinstance(q, SamplePoints) else to_sample_based(
+                q, T, [c.seed, STREAM_REFERENCE])
+            targets.append(np.asarray(tg.points, dtype=np.float64))
+        M = targets[0].shape[0]
+        eligible = all(t.shape == (M, d) for t in targets)
+    if eligible:
+        prec = _precision.pick(cfg.sinkhorn.precision, T * max(T, M), cfg.sinkhorn.tol)
+        eligible = prec == _lib.FCB_FP32
+    if not eligible:
+        return [plan_detailed(*p) for p in problems]
+
+    B = len(problems)
+    lib = _lib.load()
+    dev = _dev.require_cuda()
+    stream = _dev.stream()
+    t_begin = time.perf_counter()
+    n_s, m_c = model.state_dim, model.control_dim
+    maxit = cfg.max_iterations
+    weights = workspace_weights(model.project_matrix, m_c, cfg.q_weight, cfg.r_weight)
+    clamp = cfg.control_clamp
+    if clamp is not None and len(clamp) != m_c:
+        raise ValueError(f"control_clamp needs {m_c} bounds, got {len(clamp)}")
+    bounds = np.asarray(clamp, dtype=np.float64) if clamp is not None else None
+    U0 = np.stack([initial_controls(c, m, T) for m, _, _, c in problems])
+    if bounds is not None:
+        np.clip(U0, -bounds, bounds, out=U0)
+    s0 = _dev.f64(np.stack([ds.s0 for _, _, ds, _ in problems]), dev)
+    Yd = _dev.f64(np.stack(targets), dev)
+    Ubuf = [_dev.f64(U0, dev), _dev.zeros((B, T, m_c), device=dev)]
+    Sbuf = [_dev.zeros((B, T + 1, n_s), device=dev), _dev.zeros((B, T + 1, n_s), device=dev)]
+    X = _dev.zeros((B, T, d), device=dev)
+    flow = _dev.zeros((B, T, d), device=dev)
+    P = _dev.f64(model.project_matrix, dev)
+    Q = _dev.f64(weights.Q, dev)
+    R = _dev.f64(weights.R, dev)
+    clamp_d = _dev.f64(bounds, dev) if bounds is not None else None
+    prm = spec.device_params(dev)
+    state = torch.zeros((B, 8), dtype=torch.int32, device=dev)
+    flow_log = _dev.zeros((B, maxit, 4), device=dev)
+    lqr_costs = _dev.zeros((B, maxit), device=dev)
+    fstat = _dev.zeros((B, 8), device=dev)
+    warm_f, warm_p = _dev.zeros((B, T), device=dev), _dev.zeros((B, T), device=dev)
+    warm_valid = torch.zeros((B, 2), dtype=torch.int32, device=dev)
+    phase_ns = torch.zeros((B, 3), dtype=torch.int64, device=dev)
+    scfg = cfg.sinkhorn
+
+    def call(name, *args):
+        _lib.check(getattr(lib, name)(*args), name)
+
+    # the stored Riccati phase: the built-in linear models' Jacobians are
+    # state-independent, so one mode-0 update on scratch inputs computes it
+    upd_ws = _dev.Workspace.get(lib.fcb_plan_update_workspace_bytes(n_s, m_c, T), "batch_upd")
+    scratch_state = torch.zeros(8, dtype=torch.int32, device=dev)
+    call("fcb_plan_update", spec.model_id, n_s, m_c, _dev.ptr(prm),
+         _dev.ptr(_dev.zeros((T + 1, n_s), device=dev)), _dev.ptr(_dev.zeros((T, m_c), device=dev)),
+         T, float(disc.dt), d, _dev.ptr(P), _dev.ptr(_dev.zeros((T, d), device=dev)), _dev.ptr(Q),
+         _dev.ptr(R), float(cfg.eta), _dev.ptr(clamp_d),
+         _dev.ptr(_dev.zeros((T, m_c), device=dev)), _dev.ptr(_dev.zeros((maxit,), device=dev)),
+         _dev.ptr(scratch_state), 0, 0, _dev.ptr(upd_ws), upd_ws.numel(), stream)
+    fws = _dev.Workspace.get(lib.fcb_plan_fused_workspace_bytes(B, T, M, d, m_c), "batch_fused")
+    launches0 = lib.fcb_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rc = lib.fcb_plan_fused(
+        spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0), _dev.ptr(Ubuf[0]),
+        _dev.ptr(Ubuf[1]), _dev.ptr(Sbuf[0]), _dev.ptr(Sbuf[1]), T, float(disc.dt), d,
+        _dev.ptr(P), _dev.ptr(X), _dev.ptr(flow), _dev.ptr(Q), _dev.ptr(R), float(cfg.eta),
+        _dev.ptr(clamp_d), _dev.ptr(Yd), M, _omega_arg(scfg.omega), scfg.max_iters, scfg.tol,
+        float(cfg.convergence_tol), _dev.ptr(warm_f), _dev.ptr(warm_p), _dev.ptr(warm_valid),
+        _dev.ptr(fstat), _dev.ptr(state), _dev.ptr(flow_log), _dev.ptr(lqr_costs),
+        _dev.ptr(phase_ns), 0, maxit, B, _dev.ptr(upd_ws), _dev.ptr(fws), fws.numel(), stream)
+    if rc == _lib.FCB_ENOTSUP:
+        return [plan_detailed(*p) for p in problems]
+    _lib.check(rc, "fcb_plan_fused")
+    e1 = torch.cuda.Event(enable_timing=True)
+    e1.record()
+    e1.synchronize()
+    st_all = state.cpu().numpy()
+    logs = flow_log.cpu().numpy()
+    costs_all = lqr_costs.cpu().numpy()
+    pn_all = phase_ns.cpu().numpy().astype(np.float64) * 1e-9
+    fst = fstat.cpu().numpy()
+    roll_ws = _dev.Workspace.get(lib.fcb_rollout_workspace_bytes(n_s, T), "batch_roll")
+    runs: list[PlanRun] = []
+    for b in range(B):
+        stop_kind, stage_code, fail_it, fail_idx, flows_used, updates = (
+            int(v) for v in st_all[b, :6])
+
+        def trajectory_of(k: int, b=b) -> Trajectory | None:
+            if k < 0:
+                return None
+            return Trajectory(S=_dev.host(Sbuf[k & 1][b]).copy(),
+                              U=_dev.host(Ubuf[k & 1][b]).copy(), dt=disc.dt)
+
+        if stop_kind == 2:
+            if stage_code == 1:
+                raise PlanError("rollout", fail_it, trajectory_of(fail_it - 1),
+                                RolloutDivergenceError(fail_idx))
+            if stage_code == 2:
+                raise PlanError("flow", fail_it, trajectory_of(fail_it),
+                                FlowError(flow_error_message(float(fst[b, 0]), scfg.tol)))
+            raise PlanError("lqr", fail_it, trajectory_of(fail_it),
+                            RiccatiDivergenceError(fail_idx))
+        # final rollout on the last controls (optimizer.py:271-277)
+        U_final = Ubuf[updates & 1][b]
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+        S_final = _dev.zeros((T + 1, n_s), device=dev)
+        Xb = _dev.zeros((T, d), device=dev)
+        call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0[b]),
+             _dev.ptr(U_final), T, float(disc.dt), _dev.ptr(S_final), d, _dev.ptr(P),
+             _dev.ptr(Xb), _dev.ptr(status), None, 0, rollout_method(T), _dev.ptr(roll_ws),
+             stream)
+        fstep = int(status.item())
+        if fstep >= 0:
+            raise PlanError("rollout", updates, trajectory_of(flows_used - 1),
+                            RolloutDivergenceError(fstep))
+        log = logs[b, :flows_used].copy()
+        result = PlanResult(
+            trajectory=Trajectory(S=_dev.host(S_final).copy(), U=_dev.host(U_final).copy(),
+                                  dt=disc.dt),
+            converged=stop_kind == 1,
+            iterations_used=flows_used,
+            flow_norms=log[:, 0].copy(),
+            lqr_costs=costs_all[b, :updates].copy(),
+            metric_iterations=(),
+            metric_values=(),
+            phase_times=PhaseTimes(flow=float(pn_all[b, 1]), lqr=float(pn_all[b, 2]),
+                                   rollout=float(pn_all[b, 0]),
+                                   total=time.perf_counter() - t_begin),
+            final_metric=None,
+        )
+        runs.append(PlanRun(result=result, flow_log=log, precision=prec,
+                            pairs=_pair_count(cfg.method, log, T, M),
+                            launches=int(lib.fcb_launch_count() - launches0)))
+    return runs
+
+
+def plan_batch(problems: list) -> list[PlanResult]:
+    """plan() of every problem (batched on the device when they share a shape)."""
+    return [r.result for r in plan_batch_detailed(problems)]
