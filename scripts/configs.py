@@ -108,26 +108,46 @@ def cfg4s():
                 seconds_per_flow=t, pairs_per_s=1e10 / t, frac_of_mufu=1e10 / t / pk)
 
 
-def cfg5(problems=8):
-    """Config 5 sample: independent T=1000, M=4096 problems on one GPU, 100 iterations."""
+def cfg5(problems=512, iters=100):
+    """Config 5: independent T=1000, M=4096 single-integrator problems (problem b: seed b,
+    targets from stream [b, 2]), 512 per GPU as in SURVEY 8(d), planned as ONE batched
+    fused launch (one problem per CTA); a few problems through the per-problem loop
+    for comparison."""
     m = fc.single_integrator_2d()
     q = fc.benchmark_mixture(2)
     probs = []
     for b in range(problems):
         Y = q.sample(4096, [b, 2])
         probs.append((m, fc.SamplePoints(Y), fc.Discretization(0.05, 1000, np.array([0.1, 0.1])),
-                      fc.PlanConfig(method="sinkhorn", eta=150.0, max_iterations=100,
+                      fc.PlanConfig(method="sinkhorn", eta=150.0, max_iterations=iters,
                                     convergence_tol=0.0, metric_interval=0, seed=b)))
-    from paper_2511_11514_b200.distributed import plan_batch
-
-    plan_batch(probs[:1])
+    fc.plan_batch_detailed(probs[:2])  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    runs = fc.plan_batch_detailed(probs)
+    e1.record()
+    e1.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    pairs = sum(r.pairs for r in runs)
+    pk = peak()
+    # per-problem loop (one problem over the whole GPU at a time) on a sample
+    os.environ["FCB_FUSED"] = "0"
+    k = 4
+    fc.plan_detailed(*probs[0])
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    plan_batch(probs)
-    t = time.perf_counter() - t0
-    return dict(config=f"5 (sample): {problems} independent SI problems, T=1000, M=4096, 100 it",
-                seconds=t, seconds_per_problem=t / problems,
-                extrapolated_512_per_gpu_s=t / problems * 512)
+    seq = [fc.plan_detailed(*p) for p in probs[:k]]
+    torch.cuda.synchronize()
+    t_seq = (time.perf_counter() - t0) / k
+    os.environ["FCB_FUSED"] = "1"
+    return dict(config=f"5: {problems} independent SI problems, T=1000, M=4096, {iters} it "
+                       "(batched fused launch, one problem per CTA)",
+                seconds=t, problems_per_s=problems / t, planner_iters_per_s=problems * iters / t,
+                pairs=pairs, pairs_per_s=pairs / t, frac_of_mufu=pairs / t / pk, mufu_peak=pk,
+                per_problem_loop_seconds_per_problem=t_seq,
+                per_problem_loop_extrapolated_s=t_seq * problems,
+                seq_pairs_per_s=sum(r.pairs for r in seq) / (t_seq * k))
 
 
 if __name__ == "__main__":
