@@ -94,6 +94,38 @@ template <int N, bool FWD, class MapFn>
 __device__ AMap<N>* pf_phase1(int T, const PfChunk& ch, const MapFn& mapf, PfSmem<N>& sm,
                               double* agg_pub) {
     const int t = threadIdx.x;
+    if (ch.nact <= 32) {
+        // one warp: runs in lanes, inclusive scan by shuffles (no block syncs)
+        if (t < 32) {
+            AMap<N> acc;
+            amap_identity(acc);
+            if (t < ch.nact) {
+                AMap<N> m, tmp;
+                const int pa = ch.p0 + t * ch.L, pb = min(pa + ch.L, ch.p0 + ch.cnt);
+                for (int p = pa; p < pb; ++p) {
+                    mapf(FWD ? p : T - 1 - p, m);
+                    amap_compose(m, acc, tmp);
+                    acc = tmp;
+                }
+            }
+#pragma unroll 1
+            for (int o = 1; o < 32; o <<= 1) {
+                AMap<N> prev, tmp;
+                amap_shfl(prev, acc, o, true);
+                if (t >= o) {
+                    amap_compose(acc, prev, tmp);
+                    acc = tmp;
+                }
+            }
+            if (t < ch.nact) sm.run[0][t] = acc;
+            if (agg_pub && t == max(ch.nact - 1, 0)) {
+                if (ch.nact == 0) amap_identity(acc);
+                amap_copy_to(agg_pub + (size_t)ch.c * (N * N + N), acc);
+            }
+        }
+        __syncthreads();
+        return sm.run[0];
+    }
     if (t < ch.nact) {
         AMap<N> acc, m, tmp;
         amap_identity(acc);
@@ -117,6 +149,42 @@ __device__ AMap<N>* pf_phase1(int T, const PfChunk& ch, const MapFn& mapf, PfSme
     return inc;
 }
 
+// Composition A_{c-1} o ... o A_0 of the first c published chunk aggregates:
+// warps load 32 maps each, an ordered shuffle tree (lane i absorbs lane i+o,
+// the later map) reduces each warp, thread 0 chains the warp results.
+template <int N>
+__device__ void pf_carry(const double* agg_pub, int c, PfSmem<N>& sm, AMap<N>& out) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int nw = (c + 31) >> 5;
+    if (w < nw) {
+        AMap<N> mine;
+        const int i = w * 32 + lane;
+        if (i < c) amap_copy_from(agg_pub + (size_t)i * (N * N + N), mine);
+        else amap_identity(mine);
+#pragma unroll 1
+        for (int o = 1; o < 32; o <<= 1) {
+            AMap<N> later, tmp;
+            amap_shfl(later, mine, o, false);
+            if ((lane & (2 * o - 1)) == 0) {
+                amap_compose(later, mine, tmp);
+                mine = tmp;
+            }
+        }
+        if (lane == 0) sm.car[0][w] = mine;
+    }
+    __syncthreads();
+    if (t == 0) {
+        AMap<N> acc = sm.car[0][0];
+        for (int k = 1; k < nw; ++k) {
+            const AMap<N> nxt = sm.car[0][k];
+            AMap<N> tmp;
+            amap_compose(nxt, acc, tmp);
+            acc = tmp;
+        }
+        out = acc;
+    }
+}
+
 // Phase 2: the chunk's start state (init carried over the earlier chunks'
 // aggregates), then every run steps through its positions calling
 // out(k, x_k, x_k+1) (states in scan order).  Returns the thread's sum of out.
@@ -126,14 +194,12 @@ __device__ double pf_phase2(int T, const PfChunk& ch, const MapFn& mapf, const O
                             const double* agg_pub) {
     const int t = threadIdx.x;
     if (GRID && ch.c > 0) {
-        for (int i = t; i < ch.c; i += RS_BLOCK) amap_copy_from(agg_pub + (size_t)i * (N * N + N), sm.car[0][i]);
-        __syncthreads();
-        const AMap<N>* pre = pf_scan<N>(sm.car[0], sm.car[1], ch.c);
+        AMap<N> pm;
+        pf_carry<N>(agg_pub, ch.c, sm, pm);
         if (t == 0) {
             double x0[N], x1[N];
 #pragma unroll
             for (int i = 0; i < N; ++i) x0[i] = init ? init[i] : 0.0;
-            const AMap<N> pm = pre[ch.c - 1];
             amap_apply(pm, x0, x1);
 #pragma unroll
             for (int i = 0; i < N; ++i) sm.xs[i] = x1[i];
