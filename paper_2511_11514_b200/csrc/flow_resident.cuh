@@ -122,6 +122,7 @@ struct RsArgs {
     int ldA, ldB;             // floats per array of smem regions A and B
     int cache_off, cache_rows;  // own-row cache (floats offset, rows; 0: none)
     unsigned launch_id;         // grid groups: epoch of this launch (barrier reset)
+    const double* ystat;        // nullable: precomputed target moments [4]
 };
 
 // Shared-memory column set: D coordinate arrays and the folded potential,
@@ -526,7 +527,13 @@ struct RsRows {
     __device__ __forceinline__ double potential(int li) const {
         return cache ? cache[li].pot : __ldcg(pot + base + li);
     }
-    __device__ __forceinline__ double shift2(double pv) const { return kLog2e * (logw - pv * inv_w); }
+    // the row's LSE estimate from a potential; a non-finite potential (an
+    // estimate taken from stale memory) means no estimate -- the careful pass
+    // then finds the shift, so an estimate never changes a result
+    __device__ __forceinline__ double shift2(double pv) const {
+        const double e = kLog2e * (logw - pv * inv_w);
+        return isfinite(e) ? e : 0.0;
+    }
     __device__ __forceinline__ void init(int li, float* x, float& rc) const {
         if (cache) {
             const RsCache& e = cache[li];
@@ -633,6 +640,27 @@ __device__ __forceinline__ double rs_ordered_sum(const double* v, int n) {
     return warp_sum(s);
 }
 
+// Block-wide moments of a point set (sums of coordinates, sum of |p|^2) in a
+// fixed order: out[0..D), out[3]; every thread calls it.
+template <int D>
+__device__ __forceinline__ void rs_block_moments(const double* P, int cnt, double (*red)[8],
+                                                 double* out) {
+    double acc[4] = {0, 0, 0, 0};
+    rs_moments<D>(P, cnt, acc);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double v = warp_sum(acc[k]);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double v = 0.0;
+        for (int w = 0; w < RS_WARPS; ++w) v += red[w][threadIdx.x];
+        out[threadIdx.x] = v;
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ double rs_nanmax(double a, double b) { return (b > a || b != b) ? b : a; }
 
 // ---------------------------------------------------------------------------
@@ -695,22 +723,14 @@ __device__ __forceinline__ void rs_flow_body(const RsArgs& A, bool wait_epoch) {
     RS_MARK(0);
 
     // ---- statistics (every CTA, fixed order) -> omega, centres -------------
-    {
-        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        rs_moments<D>(X, n, acc);
-        rs_moments<D>(Y, m, acc + 4);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const double v = warp_sum(acc[k]);
-            if ((tid & 31) == 0) s_red[tid >> 5][k] = v;
-        }
+    // (A.ystat: the target statistics, fixed across the flows of a planner
+    // launch, computed once by the caller with this same reduction)
+    rs_block_moments<D>(X, n, s_red, s_sum);
+    if (A.ystat) {
+        if (tid < 4) s_sum[4 + tid] = A.ystat[tid];
         __syncthreads();
-        if (tid < 8) {
-            double v = 0.0;
-            for (int w = 0; w < RS_WARPS; ++w) v += s_red[w][tid];
-            s_sum[tid] = v;
-        }
-        __syncthreads();
+    } else {
+        rs_block_moments<D>(Y, m, s_red, s_sum + 4);
     }
     double mx[3] = {0, 0, 0}, my[3] = {0, 0, 0}, dot = 0.0;
 #pragma unroll
@@ -776,6 +796,8 @@ __device__ __forceinline__ void rs_flow_body(const RsArgs& A, bool wait_epoch) {
         cacheY = cbase;
         cacheX = cbase + yn;
         cacheS = cbase + yn + xn;
+        // no estimate for sweep A's first pass (g does not exist yet; an
+        // estimate from stale memory would make results depend on it)
         RsRows<D>{Y, yj0, cA, sd, nullptr, logb, inv_w, cacheY}.fill(yn, nullptr);
         RsRows<D>{X, xi0, cA, sd, nullptr, loga, inv_w, cacheX}.fill(xn, vf ? warm_f : nullptr);
         RsRows<D>{X, xi0, cB, sd, nullptr, loga, inv_w, cacheS}.fill(xn, vp ? warm_p : nullptr);

@@ -318,6 +318,12 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
     double* X = const_cast<double*>(A0.X) + oTd;
     double* lqr_costs = pf.lqr_costs + (size_t)b * pf.maxit;
     const LiftedFlow<N> lift{flow, pf.P, pf.d};
+    // target moments: fixed for the launch (the flows reuse them)
+    __shared__ double s_ystat[4];
+    {
+        __shared__ double s_red8[RS_WARPS][8];
+        rs_block_moments<D>(A0.Y + (size_t)b * A0.m * D, A0.m, s_red8, s_ystat);
+    }
     bool first = true;
     bool pending_finish = false;
     int pending_it = 0;
@@ -367,6 +373,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
         {
             RsArgs A = A0;
             A.iteration = it;
+            A.ystat = s_ystat;
             rs_flow_body<D, GRID>(A, false);
         }
         const unsigned long long t2 = pf_clock();
