@@ -145,13 +145,31 @@ struct RsRes {  // combined row partial
 
 
 
+// Barriers passed by this CTA in the current launch (grid groups): the
+// arrival target is known locally, so an arrival is a fire-and-forget
+// red.release (no atomic round trip) and only the poll waits.
+__shared__ unsigned rs_bar_gen;
+
 template <bool GRID>
 struct RsGroup {
     int rank, size;
     GridBarrier* bar;
     __device__ __forceinline__ void sync() const {
-        if constexpr (GRID) grid_sync(bar);
-        else __syncthreads();
+        if constexpr (GRID) {
+            __syncthreads();
+            FCB_TL_MARK();
+            if (threadIdx.x == 0) {
+                const unsigned target = (rs_bar_gen + 1u) * (unsigned)size;
+                rs_bar_gen += 1u;
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&bar->count)
+                             : "memory");
+                while (ld_acquire_u32(&bar->count) < target) __nanosleep(20);
+            }
+            __syncthreads();
+            FCB_TL_MARK();
+        } else {
+            __syncthreads();
+        }
     }
 };
 
@@ -672,6 +690,7 @@ unsigned next_launch_epoch();  // flow_resident.cu
 // publishes the launch epoch; the others wait for it before their first
 // arrival, so no host-side memset is needed between launches.
 __device__ __forceinline__ void rs_start_epoch(const RsArgs& A) {
+    if (threadIdx.x == 0) rs_bar_gen = 0u;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         A.bar->count = 0u;
         *A.done = 0u;
