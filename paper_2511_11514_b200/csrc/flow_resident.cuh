@@ -182,6 +182,35 @@ __device__ __forceinline__ void rs_reload(const RsCols& cs, const float* src) {
     for (int j = threadIdx.x; j < cs.nq; j += RS_BLOCK) d4[j] = __ldcg(s4 + j);
 }
 
+// exp2 of a packed pair on the FMA pipe (offloads the MUFU queue in the pair
+// loop): t = j + f with j = rint(t), f in [-1/2, 1/2]; 2^f by a degree-5
+// near-minimax polynomial (relative error 3.5e-7 in fp32, MUFU.EX2's is
+// ~2.4e-7) and 2^j added into the exponent field.  t is clamped to
+// [-127, 127]: 2^-127 comes out as exactly 0 (the -inf padding columns), and
+// the exponent never wraps.  Off by default: measured in scripts/micro/
+// rs_loop.cu, offloading one pair in four is neutral for the plain sweeps and
+// 10-15 points slower for the moment sweeps (the loop is issue-bound there,
+// not MUFU-bound).
+#ifndef RS_EMU
+#define RS_EMU 0
+#endif
+__device__ __forceinline__ float2 rs_ex2_poly2(float2 t) {
+    t.x = fminf(fmaxf(t.x, -127.f), 127.f);
+    t.y = fminf(fmaxf(t.y, -127.f), 127.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+    const float2 y = __fadd2_rn(t, magic);
+    const float2 j = __fadd2_rn(y, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __fadd2_rn(t, make_float2(-j.x, -j.y));
+    float2 p = make_float2(0.0012915670f, 0.0012915670f);
+    p = __ffma2_rn(p, f, make_float2(0.0096685309f, 0.0096685309f));
+    p = __ffma2_rn(p, f, make_float2(0.055516887f, 0.055516887f));
+    p = __ffma2_rn(p, f, make_float2(0.24022265f, 0.24022265f));
+    p = __ffma2_rn(p, f, make_float2(0.69314647f, 0.69314647f));
+    p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(y.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(y.y) << 23)));
+}
+
 // A row sum is trusted in [2^-64, 2^120]: below, nothing has been
 // accumulated under a too-high shift estimate; above (or inf / NaN), the
 // terms overflowed.  Positive floats order like their bit patterns, so the
@@ -343,7 +372,9 @@ __device__ __forceinline__ void rs_rows(const RsCols& cols, int cg_log, const Rs
                 for (int q = 0; q < D; ++q)
                     t = __ffma2_rn(make_float2(x[r][q], x[r][q]),
                                    make_float2(y[q][2 * u], y[q][2 * u + 1]), t);
-                e[u] = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+                // one pair in four on the FMA pipe, three on MUFU.EX2
+                if (RS_EMU && u == 3) e[u] = rs_ex2_poly2(t);
+                else e[u] = make_float2(ex2_approx(t.x), ex2_approx(t.y));
             }
             s2[r] = __fadd2_rn(s2[r], __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3])));
             if constexpr (BARY) {
