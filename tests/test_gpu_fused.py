@@ -112,3 +112,16 @@ def test_batched_problems_match_individual_plans(model_name):
         assert rel_inf(got.result.flow_norms, ref.result.flow_norms) <= 1e-4
         assert rel_inf(got.result.lqr_costs, ref.result.lqr_costs) <= 1e-4
         assert np.abs(got.flow_log[:, 1:3] - ref.flow_log[:, 1:3]).max() <= 1
+
+
+def test_bench_plugin_runs_planners():
+    from types import SimpleNamespace
+
+    from paper_2511_11514_b200 import bench_plugin
+
+    spec = SimpleNamespace(model="single_integrator_2d", dt=0.05, seed=0, plan=None)
+    planners = bench_plugin.b200_planners(spec)
+    for name in ("b200-stein", "b200-sinkhorn"):
+        run = planners[name](60, 1)
+        assert run.trajectory.S.shape == (61, 2)
+        assert run.t_flow > 0 and run.t_lqr >= 0 and run.t_rollout > 0

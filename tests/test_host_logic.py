@@ -124,3 +124,16 @@ def test_compute_entry_points_fail_loudly_without_a_gpu():
         fc.sinkhorn_flow(np.random.rand(5, 2), fc.SamplePoints(np.random.rand(6, 2)))
     with pytest.raises(_lib.NativeLibraryError):
         fc.rollout(fc.single_integrator_2d(), np.zeros(2), np.ones((3, 2)), 0.1)
+
+
+def test_bench_plugin_planners_build_without_gpu():
+    """bench_plugin mirrors the reference harness's planner closures (bench.py:158-209)."""
+    from types import SimpleNamespace
+
+    from paper_2511_11514_b200 import bench_plugin
+
+    spec = SimpleNamespace(model="diff_drive", dt=0.05, seed=3, plan=None)
+    planners = bench_plugin.b200_planners(spec)
+    assert set(planners) == {"b200-stein", "b200-sinkhorn"}
+    assert all(callable(p) for p in planners.values())
+    assert bench_plugin.STUDY_ITERATIONS == 20 and bench_plugin.STUDY_BANDWIDTH == 0.02
