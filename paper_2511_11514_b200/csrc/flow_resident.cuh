@@ -109,6 +109,8 @@ struct RsArgs {
     double* gbuf;      // m
     float* WX;         // grid groups: published folded potentials
     float* WY;
+    float* WS;         // self term: 2 published buffers per problem (ldWS floats each)
+    int ldWS;
     double* dx;        // n: delta of the last cross update
     double* bx;        // n (D + 1): log plan row mass, barycentre
     double* dp;        // n: the same for the self term
@@ -857,6 +859,13 @@ __device__ __forceinline__ void rs_flow_body(const RsArgs& A, bool wait_epoch) {
         for (int j = m + tid; j < colB.nq * 4; j += RS_BLOCK) A.WY[j] = -INFINITY;
         for (int i = n + tid; i < colA.nq * 4; i += RS_BLOCK) A.WY[i] = -INFINITY;
     }
+    if (!GRID || grp.rank == 0) {  // padding of the self term's published buffers
+        float* WSb = A.WS + (size_t)b * 2 * A.ldWS;
+        for (int i = n + tid; i < A.ldWS; i += RS_BLOCK) {
+            WSb[i] = -INFINITY;
+            WSb[A.ldWS + i] = -INFINITY;
+        }
+    }
     if (tid == 0 && (!GRID || grp.rank == 0)) {
         errslot[0] = 0ull;
         errslot[1] = 0ull;
@@ -964,14 +973,18 @@ __device__ __forceinline__ void rs_flow_body(const RsArgs& A, bool wait_epoch) {
         double* pcur = pbuf + (size_t)pc * n;
         double* pnxt = pbuf + (size_t)(pc ^ 1) * n;
         unsigned long long* slot = errslot + ((itA + it) % 3);
-        // grid groups alternate the published array: a fast CTA must not
-        // overwrite what a slow one is still reloading
-        float* pub = (it & 1) ? A.WY : A.WX;
-        const float* prev = (it & 1) ? A.WX : A.WY;
+        // The self update reads and writes the same column set, so the new
+        // folded potentials always go to a global buffer (double-buffered: a
+        // fast CTA must not overwrite what a slow one is still reloading) and
+        // are reloaded by the next iteration -- every update of an iteration
+        // reads the previous iterate, as sinkhorn.py:225-231 does.
+        float* WSb = A.WS + (size_t)b * 2 * A.ldWS;
+        float* pub = WSb + (size_t)(it & 1) * A.ldWS;
+        const float* prev = WSb + (size_t)((it & 1) ^ 1) * A.ldWS;
         double emax = 0.0;
         {
             const RsRows<D> rows{X, xi0, cB, sd, pcur, loga, inv_w, cacheS};
-            float* wX = GRID ? pub : rs_smem + colB.w;
+            float* wX = pub;
             const double csc = 2.0 * sd;
             rs_sweep<D, true>(colB, xn, A.plS, rows,
                               [&](int li, double L, const double* bar) {
@@ -991,7 +1004,7 @@ __device__ __forceinline__ void rs_flow_body(const RsArgs& A, bool wait_epoch) {
                                   wX[i] = (float)(sd * nxt + rows.rowc2(li));
                                   rows.set_next(li, nxt);
                               },
-                              s_res, s_xw, (GRID && it > 1) ? prev : nullptr, 40);
+                              s_res, s_xw, it > 1 ? prev : nullptr, 40);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) emax = rs_nanmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
@@ -1169,7 +1182,8 @@ static RsPlan rs_pick_plan(int rows, int cols, int d, bool bary, int smem_quads_
 
 struct RsWs {
     double *fbuf, *pbuf, *gbuf, *dx, *bx, *dp, *bp, *fin_part;
-    float *WX, *WY;
+    float *WX, *WY, *WS;
+    int ldWS;
     unsigned long long* errslot;
     unsigned* done;
     GridBarrier* bar;
@@ -1194,6 +1208,8 @@ static RsWs rs_layout(int batch, int n, int m, int d, int group, void* ws, size_
     const int nw = 4 * std::max((n + 3) / 4, (m + 3) / 4);
     L.WX = ar.take<float>(nw);
     L.WY = ar.take<float>(nw);
+    L.ldWS = 4 * ((n + 3) / 4);
+    L.WS = ar.take<float>(B * 2 * (size_t)L.ldWS);
     L.total = ar.off + 256;
     return L;
 }
@@ -1252,6 +1268,8 @@ static void rs_fill(RsArgs& a, const RsWs& L, const RsShape& sh) {
     a.gbuf = L.gbuf;
     a.WX = L.WX;
     a.WY = L.WY;
+    a.WS = L.WS;
+    a.ldWS = L.ldWS;
     a.dx = L.dx;
     a.bx = L.bx;
     a.dp = L.dp;
