@@ -890,7 +890,17 @@ static int plan_fused_t(const double* prm, const double* s0, double* U0, double*
         if (G > PF_CARRY) return fail(FCB_ENOTSUP, "too many SMs for the fused planner");
         const RsShape sh = rs_shape(T, M, d, G, grid_mode);
         if (!sh.ok) return fail(FCB_ENOTSUP, "point sets do not fit in shared memory");
-        const size_t smem = std::max(sh.smem, pf_smem_bytes<N>());
+        size_t smem = std::max(sh.smem, pf_smem_bytes<N>());
+        int const_off = 0;
+        if (grid_mode) {  // per-CTA copy of the stored Riccati arrays
+            const size_t cmax = (size_t)(T + G - 1) / G;
+            const size_t cbytes = cmax * (N * N + 3 * MC * N) * sizeof(double);
+            const size_t off = align_up(smem, 16);
+            if (off + cbytes + RS_STATIC_SMEM <= (size_t)rs_smem_limit()) {
+                const_off = (int)off;
+                smem = off + cbytes;
+            }
+        }
         if (smem + RS_STATIC_SMEM > (size_t)rs_smem_limit())
             return fail(FCB_ENOTSUP, "fused planner shared memory");
         PfWs L = pf_layout(batch, T, M, d, MC, G, ws, ws_bytes);
@@ -940,6 +950,7 @@ static int plan_fused_t(const double* prm, const double* s0, double* U0, double*
         pf.S1 = S1;
         pf.lqr_costs = lqr_costs;
         pf.phase_ns = phase_ns;
+        pf.const_off = const_off;
         pf.agg = L.agg;
         pf.part = L.part;
         pf.ipart = L.ipart;

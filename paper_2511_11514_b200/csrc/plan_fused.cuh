@@ -269,6 +269,7 @@ struct PlanFusedArgs {
     double* S1;
     double* lqr_costs;
     unsigned long long* phase_ns;  // [3]: rollout, flow, LQR device time
+    int const_off;        // bytes into dynamic smem of the Riccati-array copy (0: none)
     // grid scratch
     double* agg;          // PF_CARRY maps
     double* part;         // PF_CARRY
@@ -330,6 +331,39 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
     const PfChunk chF = pf_chunk<true, GRID>(T, grp);
     const PfChunk chB = pf_chunk<false, GRID>(T, grp);
     unsigned long long tr = 0, tf = 0, tl = 0;
+    // Riccati arrays of this CTA's steps, copied once into shared memory
+    // (grid groups, few steps per CTA): the scans then build their maps
+    // without L2 round trips.  Same element-major layout with the chunk
+    // length as stride; the pointers are offset by -k0 so that the functors'
+    // (element * stride + k) indexing is unchanged.
+    const double* rAcl = pf.Acl;
+    const double* rK = pf.K;
+    const double* rLg = pf.Lg;
+    const double* rGm = pf.Gm;
+    int rstride = T;
+    if (GRID && pf.const_off > 0) {
+        double* cs = reinterpret_cast<double*>(reinterpret_cast<char*>(rs_smem) + pf.const_off);
+        const int cnt = chF.cnt;
+        double* sAcl = cs;
+        double* sK = sAcl + (size_t)N * N * cnt;
+        double* sLg = sK + (size_t)M * N * cnt;
+        double* sGm = sLg + (size_t)M * N * cnt;
+        for (int i = tid; i < N * N * cnt; i += RS_BLOCK) {
+            const int e = i / cnt, k = i - e * cnt;
+            sAcl[i] = __ldg(pf.Acl + (size_t)e * T + chF.k0 + k);
+        }
+        for (int i = tid; i < M * N * cnt; i += RS_BLOCK) {
+            const int e = i / cnt, k = i - e * cnt;
+            sK[i] = __ldg(pf.K + (size_t)e * T + chF.k0 + k);
+            sLg[i] = __ldg(pf.Lg + (size_t)e * T + chF.k0 + k);
+            sGm[i] = __ldg(pf.Gm + (size_t)e * T + chF.k0 + k);
+        }
+        rAcl = sAcl - chF.k0;
+        rK = sK - chF.k0;
+        rLg = sLg - chF.k0;
+        rGm = sGm - chF.k0;
+        rstride = cnt;
+    }
     __syncthreads();
     for (int it = pf.it0; it < pf.maxit; ++it) {
         double* U = ((it & 1) ? pf.U1 : pf.U0) + oTM;
@@ -382,7 +416,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
         if (tid == 0) {
             s_fail = -1;
         }
-        const EtaMap<N, LiftedFlow<N>> emap{pf.Acl, pf.Q, pf.dt, T, lift};
+        const EtaMap<N, LiftedFlow<N>> emap{rAcl, pf.Q, pf.dt, rstride, lift};
         const AMap<N>* incE = pf_phase1<N, false>(T, chB, emap, sm, GRID ? pf.agg : nullptr);
         RS_MARK(57);
         grp.sync();  // flow statistics and stop flags visible
@@ -391,12 +425,12 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
         __syncthreads();
         if (s_stop != 0) break;
         {
-            const EtaOut<N, M> eout{pf.Lg, dff, &s_fail, T};
+            const EtaOut<N, M> eout{rLg, dff, &s_fail, rstride};
             pf_phase2<N, false, GRID>(T, chB, emap, eout, nullptr, sm, incE, GRID ? pf.agg : nullptr);
         }
         __syncthreads();
         if (GRID && tid == 0) pf.ipart[grp.rank] = -s_fail;  // min of -fail = -max fail
-        const ZMap<N, M> zmap{pf.Acl, pf.Gm, dff, T};
+        const ZMap<N, M> zmap{rAcl, rGm, dff, rstride};
         const AMap<N>* incZ = pf_phase1<N, true>(T, chF, zmap, sm, GRID ? pf.agg + (size_t)PF_CARRY * (N * N + N) : nullptr);
         RS_MARK(59);
         grp.sync();
@@ -411,7 +445,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 1)
         }
         if (tid == 0) s_fail = -1;
         __syncthreads();
-        const ZOut<N, M, LiftedFlow<N>> zout{pf.K, T, dff, pf.Q, pf.R, pf.dt, lift, &s_fail,
+        const ZOut<N, M, LiftedFlow<N>> zout{rK, rstride, dff, pf.Q, pf.R, pf.dt, lift, &s_fail,
                                               nullptr, nullptr, U, Un, pf.eta, pf.clamp};
         const double c = pf_phase2<N, true, GRID>(T, chF, zmap, zout, nullptr, sm, incZ,
                                                   GRID ? pf.agg + (size_t)PF_CARRY * (N * N + N) : nullptr);
