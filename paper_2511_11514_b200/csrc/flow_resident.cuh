@@ -1140,7 +1140,8 @@ static int pad_quads(int nq, int cg) {
 // the pair loop is MUFU-bound from one row per thread on; what differs is the
 // padding waste (rows rounded up to nr, columns to 2 x threads) and the
 // combine cost (butterfly levels, cross-warp merge, fp64 epilogue latency).
-static RsPlan rs_pick_plan(int rows, int cols, int d, bool bary, int smem_quads_cap) {
+static RsPlan rs_pick_plan(int rows, int cols, int d, bool bary, int smem_quads_cap,
+                           double bfly = 24.0) {
     const int nq = (cols + 3) / 4;
     const int nrmax = rs_max_nr(d, bary);
     double best = 1e300;
@@ -1168,7 +1169,7 @@ static RsPlan rs_pick_plan(int rows, int cols, int d, bool bary, int smem_quads_
                 }
                 const double load = *std::max_element(smsp, smsp + 4);
                 const int kmax = q + (rem > 0 ? 1 : 0);
-                const double comb = kmax * (std::min(lg, 5) * 24.0 + (lg > 5 ? 60.0 : 0.0)) + 2500.0;
+                const double comb = kmax * (std::min(lg, 5) * bfly + (lg > 5 ? 60.0 : 0.0)) + 2500.0;
                 cost += steps * load + comb;
             }
             if (cost < best - 1e-9) {
@@ -1179,6 +1180,18 @@ static RsPlan rs_pick_plan(int rows, int cols, int d, bool bary, int smem_quads_
     }
     return pick;
 }
+
+// Tuning override of a sweep's thread layout: "<cg_log>,<rows per thread>"
+// (e.g. FCB_RS_PLAN_B=9,4); ignored unless both are in the kernel's range.
+static RsPlan rs_plan_override(const char* var, RsPlan pick, int d, bool bary) {
+    const char* v = getenv(var);
+    int lg = 0, nr = 0;
+    if (v && sscanf(v, "%d,%d", &lg, &nr) == 2 && lg >= RS_MIN_CG_LOG && lg <= 9 && nr >= 1 &&
+        nr <= rs_max_nr(d, bary))
+        return RsPlan{lg, nr};
+    return pick;
+}
+
 
 struct RsWs {
     double *fbuf, *pbuf, *gbuf, *dx, *bx, *dp, *bp, *fin_part;
@@ -1245,9 +1258,13 @@ static RsShape rs_shape(int n, int m, int d, int group, bool cache = true) {
     // generous quads cap for the plan search; checked against the limit below
     const int cap = (int)((lim - RS_STATIC_SMEM) / (4 * (d + 1)) / 4);
     const int xr = (n + group - 1) / group, yr = (m + group - 1) / group;
-    s.A = rs_pick_plan(yr, n, d, false, cap);
-    s.B = rs_pick_plan(xr, m, d, true, cap);
-    s.S = rs_pick_plan(xr, n, d, true, cap);
+    // cross sweeps: per-row butterfly levels costed at 80 (measured on B200 with
+    // scripts/layout_sweep.sh at config 2: A 16x3 / B 64x2 column threads beat
+    // the 24-cost picks 32x5 / 128x4 by 0.8 % / 1.7 % of the step); the self
+    // sweep keeps 24 (at 80 it would drop to 4 busy warps)
+    s.A = rs_plan_override("FCB_RS_PLAN_A", rs_pick_plan(yr, n, d, false, cap, 80.0), d, false);
+    s.B = rs_plan_override("FCB_RS_PLAN_B", rs_pick_plan(xr, m, d, true, cap, 80.0), d, true);
+    s.S = rs_plan_override("FCB_RS_PLAN_S", rs_pick_plan(xr, n, d, true, cap), d, true);
     s.nqpA = pad_quads((n + 3) / 4, s.A.cg);
     s.nqpB = pad_quads((m + 3) / 4, s.B.cg);
     s.nqpS = pad_quads((n + 3) / 4, s.S.cg);
