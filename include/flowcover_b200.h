@@ -80,6 +80,7 @@ enum {
 FCB_API const char* fcb_version(void);
 FCB_API const char* fcb_last_error(void);
 FCB_API long long fcb_launch_count(void); /* kernels launched by this library      */
+FCB_API const char* fcb_last_kernel(void); /* name of the last kernel launched (tests) */
 FCB_API int fcb_device_info(int* sm_count, int* cc_major, int* cc_minor);
 
 /* ---- entropic OT / Sinkhorn (sinkhorn.py) ------------------------------ */

@@ -55,6 +55,7 @@ SIGNATURES: dict[str, tuple] = {
     "fcb_version": (ctypes.c_char_p, []),
     "fcb_last_error": (ctypes.c_char_p, []),
     "fcb_launch_count": (ctypes.c_longlong, []),
+    "fcb_last_kernel": (ctypes.c_char_p, []),
     "fcb_device_info": (_I, [_P, _P, _P]),
     "fcb_omega_workspace_bytes": (_Z, [_I, _I]),
     "fcb_resolve_omega": (_I, [_I, _P, _I, _P, _I, _I, _D, _P, _P, _Z, _P]),
@@ -142,6 +143,11 @@ def last_error() -> str:
 
 def launch_count() -> int:
     return int(load().fcb_launch_count())
+
+
+def last_kernel() -> str:
+    """Name of the last kernel this library launched (path checks in tests)."""
+    return load().fcb_last_kernel().decode()
 
 
 def check(rc: int, what: str, input_error: type = ValueError) -> None:

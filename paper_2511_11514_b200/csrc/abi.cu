@@ -10,6 +10,7 @@
 namespace fcb {
 
 std::atomic<long long> g_launches{0};
+std::atomic<const char*> g_last_kernel{nullptr};
 static thread_local std::string t_last_error;
 
 void set_error(const std::string& msg) { t_last_error = msg; }
@@ -153,6 +154,10 @@ extern "C" {
 const char* fcb_version(void) { return "flowcover-b200 0.1.0 sm_100a"; }
 const char* fcb_last_error(void) { return t_last_error.c_str(); }
 long long fcb_launch_count(void) { return g_launches.load(); }
+const char* fcb_last_kernel(void) {
+    const char* k = g_last_kernel.load();
+    return k ? k : "";
+}
 
 int fcb_device_info(int* sms, int* major, int* minor) {
     int dev = 0;

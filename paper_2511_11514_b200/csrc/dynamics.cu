@@ -316,21 +316,57 @@ struct LiftedFlow {
     }
 };
 
+// The Riccati phase (lqr_split.cuh) as three launches over the whole GPU:
+// chunk aggregates + in-CTA suffix scan, the suffix scan over CTAs, and the
+// per-step re-walk emitting the gains.  The plan_* variants evaluate the
+// model's Jacobians along (S, U) on the fly and are gated by the planner
+// status word.
 template <int N, int M>
-__global__ void __launch_bounds__(LQR_THREADS) lqr_riccati_arrays_kernel(RicArgs p, const double* A,
-                                                                          const double* B) {
+__global__ void __launch_bounds__(RIC_BLOCK) ric_arrays_k1(RicArgs p, const double* A,
+                                                           const double* B) {
     ArrayJac<N, M> jac{A, B};
-    riccati_body<N, M>(jac, p);
+    riccati_k1<N, M>(jac, p);
+}
+template <int N, int M>
+__global__ void __launch_bounds__(RIC_BLOCK) ric_arrays_k3(RicArgs p, const double* A,
+                                                           const double* B) {
+    ArrayJac<N, M> jac{A, B};
+    riccati_k3<N, M>(jac, p);
+}
+
+__device__ __forceinline__ bool ric_gated(const RicArgs& p) {
+    return p.plan_state && *((volatile const int*)p.plan_state) != 0;
 }
 
 template <class Mdl>
-__global__ void __launch_bounds__(LQR_THREADS) plan_riccati_kernel(RicArgs p, const double* prm,
-                                                                    const double* S,
-                                                                    const double* U) {
-    if (p.plan_state && *((volatile int*)p.plan_state) != 0) return;
+__global__ void __launch_bounds__(RIC_BLOCK) plan_ric_k1(RicArgs p, const double* prm,
+                                                         const double* S, const double* U) {
+    if (ric_gated(p)) return;
     ModelJac<Mdl> jac{prm, S, U};
-    riccati_body<Mdl::N, Mdl::M>(jac, p);
+    riccati_k1<Mdl::N, Mdl::M>(jac, p);
 }
+template <class Mdl>
+__global__ void __launch_bounds__(RIC_BLOCK) plan_ric_k3(RicArgs p, const double* prm,
+                                                         const double* S, const double* U) {
+    if (ric_gated(p)) return;
+    ModelJac<Mdl> jac{prm, S, U};
+    riccati_k3<Mdl::N, Mdl::M>(jac, p);
+}
+
+constexpr int RIC_K2_THREADS = 512;
+
+template <int N>
+__global__ void __launch_bounds__(RIC_K2_THREADS) ric_k2(RicArgs p) {
+    if (ric_gated(p)) return;
+    riccati_k2<N>(p);
+}
+
+__global__ void ric_finish_kernel(RicArgs p) {
+    if (ric_gated(p)) return;
+    riccati_finish(p);
+}
+
+static int ric_max_blocks() { return std::min(2 * sm_count(), RIC_K2_THREADS); }
 
 // ---------------------------------------------------------------------------
 // dispatch
@@ -651,7 +687,8 @@ int linearize(int model, int ns, int m, const double* prm, const double* S, cons
 // outputs (K, H^-1 G', Acl, G; element-major), d, the affine-scan scratch, a
 // status word and the one-launch scan flags.
 struct LqrWs {
-    double *agg, *K, *Lg, *Acl, *Gm, *dff, *scan;
+    RicGeom geom;
+    double *agg, *bagg, *K, *Lg, *Acl, *Gm, *dff, *scan;
     int* fail;
     FusedWs fw;
     size_t bytes;
@@ -660,7 +697,9 @@ struct LqrWs {
 static LqrWs lqr_layout(int ns, int m, int T, void* ws) {
     Arena ar(ws, ws ? (size_t)-1 : 0);
     LqrWs L{};
-    L.agg = ar.take<double>(2 * (size_t)LQR_THREADS * 3 * ns * ns);
+    L.geom = ric_geom(T, ric_max_blocks());
+    L.agg = ar.take<double>(2 * (size_t)L.geom.nthr * 3 * ns * ns);
+    L.bagg = ar.take<double>(2 * (size_t)L.geom.nblk * 3 * ns * ns);
     L.K = ar.take<double>((size_t)T * m * ns);
     L.Lg = ar.take<double>((size_t)T * m * ns);
     L.Acl = ar.take<double>((size_t)T * ns * ns);
@@ -682,6 +721,10 @@ static RicArgs ric_args(const LqrWs& L, int T, double dt, const double* Q, const
     r.Q = Q;
     r.R = R;
     r.agg = L.agg;
+    r.bagg = L.bagg;
+    r.L = L.geom.L;
+    r.nthr = L.geom.nthr;
+    r.nblk = L.geom.nblk;
     r.K = L.K;
     r.Lg = L.Lg;
     r.Acl = L.Acl;
@@ -735,9 +778,11 @@ static int lqr_solve_t(int T, double dt, const double* A, const double* B, const
                        const double* R, const double* a, double* v, double* z, double* K,
                        double* dff, double* scal, const LqrWs& L, cudaStream_t st) {
     RicArgs r = ric_args(L, T, dt, Q, R);
-    lqr_riccati_arrays_kernel<N, M><<<1, LQR_THREADS, 0, st>>>(r, A, B);
+    ric_arrays_k1<N, M><<<r.nblk, RIC_BLOCK, 0, st>>>(r, A, B);
+    ric_k2<N><<<1, RIC_K2_THREADS, 0, st>>>(r);
+    ric_arrays_k3<N, M><<<r.nblk, RIC_BLOCK, 0, st>>>(r, A, B);
     ArrayFlow<N> fl{a};
-    int n = 1 + affine_phase<N, M>(L, L.K, dff ? dff : L.dff, T, dt, Q, R, fl, v, z, nullptr,
+    int n = 3 + affine_phase<N, M>(L, L.K, dff ? dff : L.dff, T, dt, Q, R, fl, v, z, nullptr,
                                    nullptr, 0.0, nullptr, scal, nullptr, nullptr, 0, 0, st);
     if (K) {  // gains to the caller's step-major layout [T][M][N]
         const int blocks = std::min(4 * sm_count(), (T * M * N + 255) / 256);
@@ -788,8 +833,11 @@ static int launch_plan_update(int mode, const LqrWs& L, int T, double dt, const 
         RicArgs r = ric_args(L, T, dt, Q, R);
         r.plan_state = plan_state;
         r.iteration = iteration;
-        plan_riccati_kernel<Mdl><<<1, LQR_THREADS, 0, st>>>(r, prm, S, U);
-        n = 1;
+        plan_ric_k1<Mdl><<<r.nblk, RIC_BLOCK, 0, st>>>(r, prm, S, U);
+        ric_k2<N><<<1, RIC_K2_THREADS, 0, st>>>(r);
+        plan_ric_k3<Mdl><<<r.nblk, RIC_BLOCK, 0, st>>>(r, prm, S, U);
+        ric_finish_kernel<<<1, 32, 0, st>>>(r);
+        n = 4;
     }
     // mode 1: fail := -1, the stored Riccati phase is valid
     LiftedFlow<N> fl{flow, P, d};

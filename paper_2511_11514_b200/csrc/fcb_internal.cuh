@@ -22,7 +22,13 @@ int fail(int code, const std::string& msg);
 int cuda_status(cudaError_t e, const char* where);
 extern std::atomic<long long> g_launches;
 
+extern std::atomic<const char*> g_last_kernel;
+
 inline void count_launch(long long k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+inline void count_launch_named(const char* where) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    g_last_kernel.store(where, std::memory_order_relaxed);
+}
 
 #define FCB_CUDA(call)                                              \
     do {                                                            \
@@ -32,7 +38,7 @@ inline void count_launch(long long k = 1) { g_launches.fetch_add(k, std::memory_
 
 #define FCB_LAUNCHED(where)                                         \
     do {                                                            \
-        ::fcb::count_launch();                                      \
+        ::fcb::count_launch_named(where);                           \
         cudaError_t _e = cudaGetLastError();                        \
         if (_e != cudaSuccess) return ::fcb::cuda_status(_e, where); \
     } while (0)
@@ -110,6 +116,12 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Grid-wide barrier for cooperatively launched kernels: one arrival counter
 // that only grows (the caller zeroes it before the launch).  Barrier k of the
 // launch completes when the counter reaches k * nblocks, so a CTA derives its
@@ -117,8 +129,8 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 // reset, one atomic per CTA.  Measured 1.36 us per barrier at 296 CTAs
 // against 2.4 us for a count/generation pair with full fences.
 struct GridBarrier {
-    unsigned count;
-    unsigned pad[31];   // own 128-byte line
+    unsigned long long count;  // arrivals; 64-bit so it cannot wrap within a launch
+    unsigned pad[30];   // own 128-byte line
     unsigned work;      // dynamic work-item counter (grows across phases)
     unsigned pad2[31];
 };
@@ -151,13 +163,13 @@ __device__ __forceinline__ void grid_sync(GridBarrier* b) {
     __syncthreads();
     FCB_TL_MARK();
     if (threadIdx.x == 0) {
-        const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+        const unsigned long long nb = gridDim.x * gridDim.y * gridDim.z;
         // the CTA's writes (ordered before this thread by bar.sync) are
         // released at gpu scope before the arrival
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        const unsigned old = atomicAdd(&b->count, 1u);
-        const unsigned target = (old / nb + 1u) * nb;
-        while (ld_acquire_u32(&b->count) < target) __nanosleep(20);
+        const unsigned long long old = atomicAdd(&b->count, 1ull);
+        const unsigned long long target = (old / nb + 1ull) * nb;
+        while (ld_acquire_u64(&b->count) < target) __nanosleep(20);
     }
     __syncthreads();
     FCB_TL_MARK();

@@ -150,7 +150,7 @@ struct RsRes {  // combined row partial
 // Barriers passed by this CTA in the current launch (grid groups): the
 // arrival target is known locally, so an arrival is a fire-and-forget
 // red.release (no atomic round trip) and only the poll waits.
-__shared__ unsigned rs_bar_gen;
+__shared__ unsigned long long rs_bar_gen;
 
 template <bool GRID>
 struct RsGroup {
@@ -161,11 +161,12 @@ struct RsGroup {
             __syncthreads();
             FCB_TL_MARK();
             if (threadIdx.x == 0) {
-                const unsigned target = (rs_bar_gen + 1u) * (unsigned)size;
-                rs_bar_gen += 1u;
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&bar->count)
+                // 64-bit arrival counter: no wrap within a launch
+                const unsigned long long target = (rs_bar_gen + 1ull) * (unsigned long long)size;
+                rs_bar_gen += 1ull;
+                asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&bar->count)
                              : "memory");
-                while (ld_acquire_u32(&bar->count) < target) __nanosleep(20);
+                while (ld_acquire_u64(&bar->count) < target) __nanosleep(20);
             }
             __syncthreads();
             FCB_TL_MARK();
@@ -725,7 +726,7 @@ unsigned next_launch_epoch();  // flow_resident.cu
 __device__ __forceinline__ void rs_start_epoch(const RsArgs& A) {
     if (threadIdx.x == 0) rs_bar_gen = 0u;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        A.bar->count = 0u;
+        A.bar->count = 0ull;
         *A.done = 0u;
         __threadfence();
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&A.bar->work), "r"(A.launch_id)
@@ -1261,9 +1262,12 @@ static RsShape rs_shape(int n, int m, int d, int group, bool cache = true) {
     // cross sweeps: per-row butterfly levels costed at 80 (measured on B200 with
     // scripts/layout_sweep.sh at config 2: A 16x3 / B 64x2 column threads beat
     // the 24-cost picks 32x5 / 128x4 by 0.8 % / 1.7 % of the step); the self
-    // sweep keeps 24 (at 80 it would drop to 4 busy warps)
-    s.A = rs_plan_override("FCB_RS_PLAN_A", rs_pick_plan(yr, n, d, false, cap, 80.0), d, false);
-    s.B = rs_plan_override("FCB_RS_PLAN_B", rs_pick_plan(xr, m, d, true, cap, 80.0), d, true);
+    // sweep keeps 24 (at 80 it would drop to 4 busy warps).  The 80 cost was
+    // fit on grid groups only; one-problem-per-CTA launches (group == 1, the
+    // batched planner) keep the 24 cost their layouts were measured with.
+    const double bfly = group > 1 ? 80.0 : 24.0;
+    s.A = rs_plan_override("FCB_RS_PLAN_A", rs_pick_plan(yr, n, d, false, cap, bfly), d, false);
+    s.B = rs_plan_override("FCB_RS_PLAN_B", rs_pick_plan(xr, m, d, true, cap, bfly), d, true);
     s.S = rs_plan_override("FCB_RS_PLAN_S", rs_pick_plan(xr, n, d, true, cap), d, true);
     s.nqpA = pad_quads((n + 3) / 4, s.A.cg);
     s.nqpB = pad_quads((m + 3) / 4, s.B.cg);

@@ -166,14 +166,24 @@ def _as_points(P, name: str) -> np.ndarray:
 def _check_cost_finite(X: np.ndarray, Y: np.ndarray) -> None:
     """Raise like the reference when some |x_i - y_j|^2 overflows (sinkhorn.py:277-279).
 
-    The largest squared coordinate gap is exact from the per-coordinate
-    extremes, so this costs O(n + m) instead of forming C.
+    Summing the largest gap of each coordinate gives an upper bound on every
+    C_ij in O(n + m).  For d > 1 those gaps can come from different pairs, so
+    an overflowing bound is only a hint: the exact max_ij C_ij (row blocks, no
+    (n, m) matrix) decides, as the reference's `np.isfinite(C).all()` does.
     """
     gap = np.maximum(X.max(axis=0) - Y.min(axis=0), Y.max(axis=0) - X.min(axis=0))
     with np.errstate(over="ignore", invalid="ignore"):
         bound = float((gap * gap).sum())
-    if not math.isfinite(bound):
-        raise SinkhornInputError("cost matrix has non-finite entries")
+        if math.isfinite(bound):
+            return
+        step = max(1, (1 << 22) // max(Y.shape[0], 1))
+        for lo in range(0, X.shape[0], step):
+            blk = X[lo:lo + step]
+            C = np.square(blk[:, :1] - Y[:, 0][None, :])
+            for k in range(1, X.shape[1]):
+                C += np.square(blk[:, k:k + 1] - Y[:, k][None, :])
+            if not np.isfinite(C).all():
+                raise SinkhornInputError("cost matrix has non-finite entries")
 
 
 def _dims(X: np.ndarray, Y: np.ndarray) -> None:
@@ -366,8 +376,14 @@ def sinkhorn_flow(
     cfg: SinkhornConfig = SinkhornConfig(),
     workers: int | None = None,
     warm: SinkhornWarmState | None = None,
+    *,
+    stats: dict | None = None,
 ) -> FlowField:
-    """Minus the divergence gradient at each point of X (sinkhorn.py:338-400)."""
+    """Minus the divergence gradient at each point of X (sinkhorn.py:338-400).
+
+    stats (additive, keyword-only): receives omega and the inner iteration
+    counts of the cross and self solves (iters_cross, iters_self).
+    """
     X = _as_points(X, "X")
     Y = _as_points(q.points, "reference points")
     _dims(X, Y)
@@ -392,6 +408,9 @@ def sinkhorn_flow(
     )
     st = _dev.host(fstat)
     worst = float(st[0])
+    if stats is not None:
+        stats.update(omega=float(st[4]), iters_cross=int(st[5]), iters_self=int(st[6]),
+                     worst=worst)
     if st[2] != 0.0:
         raise FlowError(flow_error_message(worst, cfg.tol))
     return FlowField(a=_dev.host(flow), converged=bool(st[1] != 0.0), marginal_error=worst)

@@ -1,0 +1,201 @@
+"""Parity of the fp32 kernels BASELINE configs 3-5 run (round-2 pins).
+
+Configs 3-4 take the chunked fp32 Sinkhorn flow (point sets too large for
+shared memory), config 4 additionally the d=3 kernels, config 5 the batched
+planner.  Each is compared here against the reference (golden plans made by
+the unmodified reference, tests/golden/make_golden_r2.py) or the oracle at
+shapes the reference cannot hold, on identical inputs:
+
+  * flows and potentials: inf-norm relative error <= 1e-4 (north_star), with
+    the inner iteration counts equal to the oracle's (at large n the stop
+    test err = max|expm1(delta)| / n <= tol is loose, so a one-iteration
+    difference would move the potentials by more than the tolerance; equal
+    counts are part of the parity claim);
+  * warm-started flows are fed the ORACLE's warm potentials so both sides
+    start from identical inputs;
+  * trajectories, controls and coverage of whole plans: <= 1%.
+
+The large inputs (X drawn from the target itself, so the flow is a small
+difference of barycentres: the cancellation of SURVEY hard part 2) are
+regenerated from seeds here; only outputs are stored.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2511_11514_b200 as fc
+from fcb_testutil import GOLDEN, load_golden, rel_inf
+from oracle import flowcover_oracle as O
+from paper_2511_11514_b200 import _lib
+from paper_2511_11514_b200.seeding import STREAM_METRIC, STREAM_REFERENCE
+
+sys.path.insert(0, GOLDEN)
+import make_golden_r2 as G  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+FLOW_TOL = 1e-4
+F32 = fc.SinkhornConfig(precision="float32")
+
+
+def _flow(X, Y, warm=None, cfg=F32):
+    st: dict = {}
+    out = fc.sinkhorn_flow(X, fc.SamplePoints(Y), cfg, warm=warm, stats=st)
+    return out, st, _lib.last_kernel()
+
+
+# ---- chunked fp32 flow at natural (non-fitting) sizes ----------------------
+@pytest.mark.parametrize("tag", ["L2", "L3"])
+def test_chunked_fp32_flow_large_cold_and_warm(tag):
+    """configs 3-4 flow kernel: T=1e4 x M=1e5 (d=2) and T=2e4 x M=2e5 (d=3)."""
+    g = load_golden("large_cases.npz")
+    X, Y = G.large_inputs(tag, O.benchmark_mixture)
+    inner = [int(v) for v in g[f"{tag}_inner"]]
+    warm = fc.SinkhornWarmState()
+    a1, st1, kern = _flow(X, Y, warm)
+    assert kern == "flow_kernel", kern  # the chunked path, not the resident one
+    assert st1["omega"] == pytest.approx(float(g[f"{tag}_omega"][0]), rel=1e-12)
+    assert (st1["iters_cross"], st1["iters_self"]) == (inner[0], inner[1])
+    assert rel_inf(a1.a, g[f"{tag}_a1"]) <= FLOW_TOL, rel_inf(a1.a, g[f"{tag}_a1"])
+    assert rel_inf(warm.f, g[f"{tag}_f1"]) <= FLOW_TOL
+    assert rel_inf(warm.p, g[f"{tag}_p1"]) <= FLOW_TOL
+    # late-iteration state: warm start from the oracle's potentials, a small step
+    warm.f, warm.p = g[f"{tag}_f1"], g[f"{tag}_p1"]
+    X2 = G.step_along(X, g[f"{tag}_a1"])
+    a2, st2, _ = _flow(X2, Y, warm)
+    assert (st2["iters_cross"], st2["iters_self"]) == (inner[2], inner[3])
+    assert rel_inf(a2.a, g[f"{tag}_a2"]) <= FLOW_TOL, rel_inf(a2.a, g[f"{tag}_a2"])
+    assert rel_inf(warm.f, g[f"{tag}_f2"]) <= FLOW_TOL
+    assert rel_inf(warm.p, g[f"{tag}_p2"]) <= FLOW_TOL
+
+
+@pytest.mark.parametrize("d,n,m", [(2, 2000, 10_000), (3, 1500, 6000), (3, 3000, 4000)])
+def test_resident_and_forced_chunked_fp32_flows_vs_oracle(monkeypatch, d, n, m):
+    """The shared-memory resident kernel (incl. rs_flow_kernel<3>) and the chunked
+    kernel forced with FCB_RESIDENT=0 on the same shapes, cold and warm."""
+    q = O.benchmark_mixture(d)
+    X, Y = q.sample(n, [21, d]), q.sample(m, [0, 2])
+    warm_o: dict = {}
+    st_o: dict = {}
+    ref1, _, _ = O.sinkhorn_flow(X, Y, warm=warm_o, workers=os.cpu_count() or 1, stats=st_o)
+    f1, p1 = warm_o["f"].copy(), warm_o["p"].copy()
+    X2 = G.step_along(X, ref1)
+    st_o2: dict = {}
+    ref2, _, _ = O.sinkhorn_flow(X2, Y, warm=warm_o, workers=os.cpu_count() or 1, stats=st_o2)
+    for resident in ("1", "0"):
+        monkeypatch.setenv("FCB_RESIDENT", resident)
+        warm = fc.SinkhornWarmState()
+        a1, st1, kern = _flow(X, Y, warm)
+        assert kern == ("rs_flow_kernel" if resident == "1" else "flow_kernel"), (resident, kern)
+        assert (st1["iters_cross"], st1["iters_self"]) == (st_o["iters_cross"], st_o["iters_self"])
+        assert rel_inf(a1.a, ref1) <= FLOW_TOL, (resident, rel_inf(a1.a, ref1))
+        assert rel_inf(warm.f, f1) <= FLOW_TOL and rel_inf(warm.p, p1) <= FLOW_TOL
+        warm.f, warm.p = f1, p1
+        a2, st2, _ = _flow(X2, Y, warm)
+        assert (st2["iters_cross"], st2["iters_self"]) == (st_o2["iters_cross"], st_o2["iters_self"])
+        assert rel_inf(a2.a, ref2) <= FLOW_TOL, (resident, rel_inf(a2.a, ref2))
+        assert rel_inf(warm.f, warm_o["f"]) <= FLOW_TOL
+        assert rel_inf(warm.p, warm_o["p"]) <= FLOW_TOL
+
+
+# ---- fp32 d=3 Stein flow -------------------------------------------------------
+def test_fp32_d3_stein_flow_median_vs_oracle():
+    q = O.benchmark_mixture(3)
+    X = q.sample(4097, [13, 3])
+    ref, h, _ = O.stein_flow(X, q, workers=os.cpu_count() or 1)
+    out = fc.stein_flow(X, fc.benchmark_mixture(3), fc.SteinConfig(precision="float32"))
+    assert out.bandwidth == h  # exact median selection
+    assert rel_inf(out.a, ref) <= FLOW_TOL, rel_inf(out.a, ref)
+
+
+def test_fp32_d3_stein_flow_fixed_h_large():
+    """config-4 SVGD kernel (fixed h, d=3) at T=2e4 vs the oracle."""
+    g = load_golden("large_cases.npz")
+    X = O.benchmark_mixture(3).sample(20_000, [12, 3])
+    out = fc.stein_flow(X, fc.benchmark_mixture(3), fc.SteinConfig(bandwidth=0.01,
+                                                                     precision="float32"))
+    assert rel_inf(out.a, g["S3_a"]) <= FLOW_TOL, rel_inf(out.a, g["S3_a"])
+
+
+# ---- whole plans on the fp32 kernels (reference golden) -------------------------
+@pytest.mark.parametrize("tag,model,method,eta,iters,T", [
+    ("dd_sk32", "diff_drive", "sinkhorn", 120.0, 20, 800),
+    ("ac_sk32", "aircraft_3d", "sinkhorn", 120.0, 15, 800),
+    ("ac_st32", "aircraft_3d", "stein", 0.1, 10, 1100),
+])
+def test_fp32_plans_vs_reference(tag, model, method, eta, iters, T):
+    g = load_golden("plan_fp32_cases.npz")
+    m = fc.get_model(model)
+    q = fc.benchmark_mixture(m.workspace_dim)
+    tg = fc.SamplePoints(q.sample(2000, [0, STREAM_REFERENCE])) if method == "sinkhorn" else q
+    cfg = fc.PlanConfig(method=method, eta=eta, max_iterations=iters, convergence_tol=0.0,
+                        metric_interval=0, seed=0)
+    run = fc.plan_detailed(m, tg, fc.Discretization(0.05, T, fc.default_start(m)), cfg)
+    assert run.precision == _lib.FCB_FP32  # "auto" picks the fp32 kernels at these sizes
+    res = run.result
+    assert res.iterations_used == iters
+    assert rel_inf(res.trajectory.S, g[f"{tag}_S"]) <= 0.01, rel_inf(res.trajectory.S, g[f"{tag}_S"])
+    assert rel_inf(res.trajectory.U, g[f"{tag}_U"]) <= 0.01
+    assert rel_inf(res.lqr_costs, g[f"{tag}_lqr_costs"]) <= 0.01
+    draws = q.sample(2000, [0, STREAM_METRIC])
+    cov = fc.coverage_metric(res.trajectory.S, m, draws)
+    assert cov == pytest.approx(float(g[f"{tag}_coverage"]), rel=0.01)
+    # per-iteration flows on the reference's own states
+    for i in range(3):
+        X, a_ref = g[f"{tag}_rec{i}_X"], g[f"{tag}_rec{i}_a"]
+        if method == "sinkhorn":
+            a = fc.sinkhorn_flow(X, tg, F32).a if i == 0 else None
+        else:
+            a = fc.stein_flow(X, q, fc.SteinConfig(precision="float32")).a
+        if a is not None:
+            assert rel_inf(a, a_ref) <= FLOW_TOL, (i, rel_inf(a, a_ref))
+
+
+def test_config3_planner_vs_oracle():
+    """config 3 (diff_drive, Sinkhorn, T=1e4, M=1e5, eta=1500): 3 outer iterations,
+    the chunked fp32 flow + on-device LTV LQR, against the oracle."""
+    g = load_golden("large_cases.npz")
+    m = fc.differential_drive()
+    Y = O.benchmark_mixture(2).sample(100_000, [0, 2])
+    cfg = fc.PlanConfig(method="sinkhorn", eta=1500.0, max_iterations=3, convergence_tol=0.0,
+                        metric_interval=0, seed=0)
+    run = fc.plan_detailed(m, fc.SamplePoints(Y), fc.Discretization(0.05, 10_000,
+                                                                    np.array([0.1, 0.1, 0.0])), cfg)
+    assert run.precision == _lib.FCB_FP32
+    assert np.array_equal(run.flow_log[:, 1:3].astype(int), g["cfg3_inner"])
+    assert rel_inf(run.result.flow_norms, g["cfg3_flow_norms"]) <= 1e-3
+    assert rel_inf(run.result.trajectory.S, g["cfg3_S"]) <= 0.01
+    assert rel_inf(run.result.lqr_costs, g["cfg3_lqr_costs"]) <= 0.01
+    # per-iteration flow on the oracle's own states
+    for i in range(3):
+        X = m.project_states(g[f"cfg3_rec{i}_S"][1:])
+        if i == 0:
+            a = fc.sinkhorn_flow(X, fc.SamplePoints(Y), F32).a
+            assert rel_inf(a, g[f"cfg3_rec{i}_a"]) <= FLOW_TOL
+
+
+# ---- config 5: batched independent problems -------------------------------------
+def test_config5_batched_vs_reference():
+    """8 problems (T=1000, M=4096) in ONE batched launch; problems 0-2 against
+    the reference's own plans."""
+    g = load_golden("batch_cfg5_cases.npz")
+    q = fc.benchmark_mixture(2)
+    model = fc.single_integrator_2d()
+    probs = []
+    for b in range(8):
+        tg = fc.SamplePoints(q.sample(4096, [b, STREAM_REFERENCE]))
+        probs.append((model, tg, fc.Discretization(0.05, 1000, np.array([0.1, 0.1])),
+                      fc.PlanConfig(method="sinkhorn", eta=150.0, max_iterations=30,
+                                    convergence_tol=0.0, metric_interval=0, seed=b)))
+    runs = fc.plan_batch_detailed(probs)
+    for b in range(3):
+        res = runs[b].result
+        assert res.iterations_used == 30
+        assert rel_inf(res.trajectory.S, g[f"b{b}_S"]) <= 0.01, (b, rel_inf(res.trajectory.S, g[f"b{b}_S"]))
+        assert rel_inf(res.trajectory.U, g[f"b{b}_U"]) <= 0.01
+        assert rel_inf(res.flow_norms, g[f"b{b}_flow_norms"]) <= 1e-3
+        assert rel_inf(res.lqr_costs, g[f"b{b}_lqr_costs"]) <= 0.01

@@ -137,3 +137,15 @@ def test_bench_plugin_planners_build_without_gpu():
     assert set(planners) == {"b200-stein", "b200-sinkhorn"}
     assert all(callable(p) for p in planners.values())
     assert bench_plugin.STUDY_ITERATIONS == 20 and bench_plugin.STUDY_BANDWIDTH == 0.02
+
+
+def test_cost_finite_check_uses_exact_pairs():
+    """sinkhorn.py:277-279 raises only when some C_ij itself overflows."""
+    from paper_2511_11514_b200.sinkhorn import SinkhornInputError, _check_cost_finite
+
+    # per-coordinate gaps overflow together, but no single pair does
+    _check_cost_finite(np.array([[1.2e154, 0.0], [0.0, 1.2e154]]), np.zeros((1, 2)))
+    with pytest.raises(SinkhornInputError):
+        _check_cost_finite(np.array([[1.2e154, 1.2e154]]), np.zeros((1, 2)))
+    with pytest.raises(SinkhornInputError):
+        _check_cost_finite(np.array([[1e200]]), np.array([[-1e200]]))
