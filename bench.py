@@ -1,44 +1,47 @@
 #!/usr/bin/env python
 """Benchmark of the reference-flow generator (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-2D double integrator, Sinkhorn-divergence flow, T=2000 trajectory states,
-M=10^4 reference samples (Gaussian-mixture draws, seed stream [0, 2]),
-200 outer planner iterations, eta=300, dt=0.05, tol=1e-6, omega="auto".
-One step = one complete plan() of that workload (rollout, flow, LQR and the
-control update for 200 iterations).
+Headline workload: BASELINE.json configs[3] -- the north_star's target shape.
+  aircraft_3d (the reference's 3D model, standing in for "quadrotor-style"),
+  T = 1e5 trajectory states, M = 1e6 reference samples (benchmark_mixture(3)
+  draws, seed stream [0, 2]), dt = 0.05, SVGD + Sinkhorn.
+  One step = 3 outer planner iterations with the Sinkhorn-divergence flow
+  (eta 15000 = 0.15 T, omega "auto", tol 1e-6, cold start) followed by 3 with
+  the SVGD flow (fixed h = 0.01, eta 0.1): rollout, flow, LQR and the control
+  update of every iteration, i.e. two complete plan() calls.
+  --gpus N (N > 1): the reference samples / SVGD sources are sharded over the
+  N ranks (distributed.py: M-sharded Sinkhorn, source-sharded SVGD) and the
+  total work is fixed -- strong scaling.  Without torchrun, bench.py launches
+  its own N ranks.
 
 metric  "flow-field pairwise evals/sec": executed (query, source) pair
-        evaluations of the LSE sweeps (2 k_a T M + k_s T^2 per outer
-        iteration, k_a / k_s the inner iteration counts the device actually
-        ran) divided by the device-timed step time; planner iterations/s
-        are reported alongside.
-value   inputs resident in HBM (targets pre-staged), CUDA events on the
-        launching stream over the K timed steps, max over ranks.
-e2e     the public plan() with host numpy inputs (uploads + result
+        evaluations -- Sinkhorn 2 k_a T M + k_s T^2 per outer iteration (k_a,
+        k_s the inner iterations the device ran), SVGD T^2 -- divided by the
+        device-timed step time (max over ranks); planner iterations/s alongside.
+value   inputs resident in HBM; CUDA events on the launching stream; a 256 MiB
+        memset between steps flushes the 126 MB L2 (inputs are smaller).
+e2e     the public plan() with host numpy inputs (target upload and result
         download inside the timed region).
-roofline  the dominant work: the Sinkhorn-flow phase of the persistent
-        planner launch (rs_plan_kernel runs iterations 1..199 in one launch;
-        iteration 0 runs rs_flow_kernel), timed live inside the timed region
-        on the device (CUDA events around the iteration-0 flow launch,
-        %globaltimer stamps around each in-kernel flow phase): executed
-        pair-evals/s (= MUFU.EX2/s, one exp2 per pair) vs the MUFU.EX2 peak
-        measured by the probe kernel in this run; traffic from the committed
-        ncu capture.
-cpu_baseline  the oracle port of the reference (numpy float64, row-chunked
-        thread pool as in the reference) on this host's cores, on a bounded
-        sample of the same workload (the first outer iterations).
+roofline  the flow phases (Sinkhorn flow_kernel, SVGD kernels), device-timed
+        inside the timed region (CUDA events around every flow launch), against
+        the composite roof of SURVEY.md §8(d): LSE-only sweeps at
+        min(MUFU, FP32/(2d+2)), barycentre/self sweeps and SVGD at
+        min(MUFU, FP32/(3d+2)); MUFU.EX2 and FFMA peaks measured live by the
+        probe kernel.  frac = (time at the roof) / (measured flow time).
+cpu_baseline  the oracle port of the reference (numpy float64, all host
+        threads) on a bounded sample of the same workload; the full step is
+        infeasible on CPU (the reference would materialise 2 TB of cost
+        matrices), so the step time is extrapolated from the sample's rate.
+secondary  BASELINE configs[1] (2D double integrator, Sinkhorn, T=2000,
+        M=1e4, 200 iterations), the round-1 headline, N=1 only.
 
---impl reference runs that CPU port as the reference arm.
---gpus N (torchrun): every rank runs its own independent problem (seed =
-rank): independent planning problems split across ranks, weak scaling.
+--impl reference runs the oracle port's sample as the reference arm.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -50,29 +53,36 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-T_STEPS = 2000
-M_TARGETS = 10_000
-ITERATIONS = 200
-ETA = 300.0
+# ---- config 4 (headline) ---------------------------------------------------------
+T4, M4, D4 = 100_000, 1_000_000, 3
+SK_ITERS, SV_ITERS = 3, 3
+ETA_SK, ETA_SV, H_SV = 15_000.0, 0.1, 0.01
 DT = 0.05
-S0 = np.array([0.1, 0.1, 0.0, 0.0])
-METRIC = "flow-field pairwise evals/sec (T x M, executed LSE sweeps)"
+METRIC = "flow-field pairwise evals/sec (T x M, executed LSE / SVGD sweeps)"
 UNIT = "pair-evals/s"
-WORKLOAD = ("2D double integrator, Sinkhorn-divergence flow, T=2000, M=1e4, 200 iterations "
-            "(BASELINE.json configs[1])")
+WORKLOAD = ("BASELINE configs[3]: aircraft_3d (3D quadrotor-style), T=1e5, M=1e6, "
+            "SVGD + Sinkhorn; step = 3 Sinkhorn-flow + 3 SVGD (fixed h) planner iterations")
+# ---- config 2 (secondary) -----------------------------------------------------------
+T2, M2, IT2, ETA2 = 2000, 10_000, 200, 300.0
+S0_DI = np.array([0.1, 0.1, 0.0, 0.0])
+# ---- CPU sample ----------------------------------------------------------------------
+CPU_ROWS, CPU_SV = 400, 8000
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def targets_for(seed: int) -> np.ndarray:
-    from paper_2511_11514_b200.reference import benchmark_mixture
+_TARGETS = []
 
-    return benchmark_mixture(2).sample(M_TARGETS, [seed, 2])
+
+def targets4():
+    if not _TARGETS:
+        from paper_2511_11514_b200.reference import benchmark_mixture
+
+        _TARGETS.append(benchmark_mixture(D4).sample(M4, [0, 2]))
+    return _TARGETS[0]
 
 
 # ---------------------------------------------------------------------------
@@ -123,7 +133,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# measurement helpers
 # ---------------------------------------------------------------------------
 def measure_peak(torch, lib, iters=4096):
     """MUFU.EX2 and FFMA throughput (ops/s) from the probe kernels."""
@@ -132,7 +142,7 @@ def measure_peak(torch, lib, iters=4096):
     out = torch.zeros(2, dtype=torch.float64, device="cuda")
     res = {}
     for which, name in ((0, "ex2"), (1, "ffma")):
-        for _ in range(2):  # warm
+        for _ in range(2):
             lib.fcb_peak_probe(which, iters, _dev.ptr(out), _dev.stream())
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -142,23 +152,27 @@ def measure_peak(torch, lib, iters=4096):
             lib.fcb_peak_probe(which, iters, _dev.ptr(out), _dev.stream())
         e1.record()
         e1.synchronize()
-        ops = float(out[0].item()) * reps
-        res[name] = ops / (e0.elapsed_time(e1) * 1e-3)
+        res[name] = float(out[0].item()) * reps / (e0.elapsed_time(e1) * 1e-3)
     return res
 
 
-def load_traffic():
-    """dram bytes per flow_kernel launch from the committed ncu --set full
-    capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "flow_kernel_traffic.json")
+def load_json(name):
     try:
-        with open(path) as fh:
-            rec = json.load(fh)
-        return rec
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
     except (OSError, ValueError):
         return None
 
 
+def sweep_pairs(run, T, M):
+    """(LSE-only pairs, barycentre-sweep pairs) of a Sinkhorn plan run."""
+    ka, ks = run.flow_log[:, 1], run.flow_log[:, 2]
+    return float((ka * T * M).sum()), float((ka * T * M + ks * T * T).sum())
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -167,19 +181,26 @@ def run_ours(args):
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", init_method="env://")
+        group = dist.group.WORLD
     else:
         torch.cuda.set_device(0)
+        group = None
     import paper_2511_11514_b200 as fc
     from paper_2511_11514_b200 import _dev, _lib
+    from paper_2511_11514_b200.distributed import shard_rows
 
     lib = _lib.load()
-    model = fc.double_integrator_2d()
-    Y = targets_for(rank)
-    disc = fc.Discretization(DT, T_STEPS, S0)
-    cfg = fc.PlanConfig(method="sinkhorn", eta=ETA, max_iterations=ITERATIONS,
-                        convergence_tol=0.0, metric_interval=0, seed=rank)
-    q = fc.SamplePoints(Y)
-    Yd = _dev.f64(Y)
+    model = fc.aircraft_3d()
+    Y = targets4()
+    Y_mine = shard_rows(Y, rank, world) if world > 1 else Y
+    q3 = fc.benchmark_mixture(D4)
+    disc = fc.Discretization(DT, T4, fc.default_start(model))
+    cfg_sk = fc.PlanConfig(method="sinkhorn", eta=ETA_SK, max_iterations=SK_ITERS,
+                           convergence_tol=0.0, metric_interval=0, seed=0)
+    cfg_sv = fc.PlanConfig(method="stein", eta=ETA_SV, max_iterations=SV_ITERS,
+                           convergence_tol=0.0, metric_interval=0, seed=0,
+                           stein=fc.SteinConfig(bandwidth=H_SV))
+    Yd = _dev.f64(Y_mine)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -194,18 +215,19 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    def sum_over_ranks(v: float) -> float:
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    def step(resident: bool):
+        if resident:
+            sk = fc.plan_detailed(model, fc.SamplePoints(Y), disc, cfg_sk, resident_targets=Yd,
+                                  group=group)
+        else:
+            sk = fc.plan_detailed(model, fc.SamplePoints(Y), disc, cfg_sk, group=group)
+        sv = fc.plan_detailed(model, q3, disc, cfg_sv, group=group)
+        return sk, sv
 
-    # ---- warm-up -------------------------------------------------------------
     for _ in range(args.warmup):
-        fc.plan_detailed(model, q, disc, cfg, resident_targets=Yd)
+        step(True)
 
-    # ---- timed: inputs resident ---------------------------------------------
+    # ---- timed: inputs resident -------------------------------------------------
     runs = []
     barrier()
     launches0 = lib.fcb_launch_count()
@@ -213,137 +235,193 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            flush.zero_()  # 256 MiB > 126 MB L2 between steps
-            runs.append(fc.plan_detailed(model, q, disc, cfg, resident_targets=Yd))
+            flush.zero_()
+            runs.append(step(True))
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
         barrier()
     launches = lib.fcb_launch_count() - launches0
-    t_dev = e0.elapsed_time(e1) * 1e-3
-    pairs_local = sum(r.pairs for r in runs)
-    t_max = max_over_ranks(t_dev)
-    pairs_all = sum_over_ranks(pairs_local)
-    iters_all = sum_over_ranks(float(sum(r.result.iterations_used for r in runs)))
+    t_max = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+    pairs = sum(sk.pairs + sv.pairs for sk, sv in runs)  # whole-job pairs (same on all ranks)
+    iters = sum(sk.result.iterations_used + sv.result.iterations_used for sk, sv in runs)
 
-    # ---- e2e: public API, host inputs -----------------------------------------
+    # ---- e2e: public plan() with host inputs ------------------------------------------
     barrier()
-    h2d = Y.nbytes + T_STEPS * 2 * 8 + S0.nbytes
-    d2h = 0
+    h2d = d2h = 0
     e2e_pairs = 0.0
     ee0 = torch.cuda.Event(enable_timing=True)
     ee0.record()
     for _ in range(args.steps):
         flush.zero_()
-        run = fc.plan_detailed(model, fc.SamplePoints(targets_for(rank)), disc, cfg)
-        res = run.result
-        d2h = (res.trajectory.S.nbytes + res.trajectory.U.nbytes + res.flow_norms.nbytes
-               + res.lqr_costs.nbytes)
-        e2e_pairs += run.pairs
+        sk, sv = step(False)
+        h2d = Y_mine.nbytes + 2 * (T4 * 3 * 8 + 6 * 8)  # targets, initial controls, s0
+        d2h = sum(r.result.trajectory.S.nbytes + r.result.trajectory.U.nbytes
+                  + r.result.flow_norms.nbytes + r.result.lqr_costs.nbytes for r in (sk, sv))
+        e2e_pairs += sk.pairs + sv.pairs
     ee1 = torch.cuda.Event(enable_timing=True)
     ee1.record()
     barrier()
     t_e2e = max_over_ranks(ee0.elapsed_time(ee1) * 1e-3)
-    e2e_pairs_all = sum_over_ranks(e2e_pairs)
 
-    # ---- roofline of the dominant kernel (live, inside the timed region) -----
-    # plan() runs iteration 0 as separate launches (rollout, rs_flow_kernel,
-    # Riccati + update) and iterations 1.. as ONE persistent rs_plan_kernel
-    # launch; the flow phase time of every iteration is device time (CUDA
-    # events around the iteration-0 flow launch, %globaltimer stamps of the
-    # flow phase inside rs_plan_kernel).  Algorithmic work: one exp2 per
-    # (query, source) pair of every executed LSE sweep.
-    roof = None
-    if rank == 0:
-        peak = measure_peak(torch, lib)
-        ex2_peak = peak["ex2"]
-        t_flow = sum(r.result.phase_times.flow for r in runs)
-        t_total = sum(r.result.phase_times.total for r in runs)
-        n_launch = sum(r.result.iterations_used for r in runs)
-        achieved = pairs_local / max(t_flow, 1e-12)
-        tr = load_traffic()
-        roof = {
-            "bound": "mufu",
-            "kernel": "rs_plan_kernel<2,1,DoubleIntegrator> flow phase (shared-memory-resident "
-                      "Sinkhorn flow: omega, packs, asymmetric + self solves, envelope gradient)",
-            "achieved": achieved / 1e9,
-            "peak": ex2_peak / 1e9,
-            "unit": "Gexp/s",
-            "frac": achieved / ex2_peak,
-            "traffic": (tr["dram_bytes_per_launch"] if tr else None),
-            "traffic_source": (tr["source"] if tr else None),
-            "algorithmic_bytes_per_launch": (tr["algorithmic_bytes_per_launch"] if tr else None),
-            "peak_source": "measured MUFU.EX2 probe (fcb_peak_probe) in this run",
-            "ffma_peak_Gops": peak["ffma"] / 1e9,
-            "algorithmic": "1 exp2 per pair; pairs/launch = 2*k_a*T*M + k_s*T^2 (executed)",
-            "launches": n_launch,
-            "pairs_per_launch": pairs_local / max(n_launch, 1),
-            "ms_per_launch": t_flow / max(n_launch, 1) * 1e3,
-            "share_of_step": t_flow / max(t_total, 1e-12),
-        }
+    # ---- roofline of the flow phases ------------------------------------------------
+    peak = measure_peak(torch, lib)
+    lse, bary = 0.0, 0.0
+    for sk, _ in runs:
+        a, b = sweep_pairs(sk, T4, M4)
+        lse += a
+        bary += b
+    svp = sum(sv.pairs for _, sv in runs)
+    roof_lse = min(peak["ex2"], peak["ffma"] / (2 * D4 + 2))
+    roof_bary = min(peak["ex2"], peak["ffma"] / (3 * D4 + 2))
+    t_roof = lse / roof_lse + (bary + svp) / roof_bary
+    t_flow_local = sum(sk.result.phase_times.flow + sv.result.phase_times.flow for sk, sv in runs)
+    t_flow = max_over_ranks(t_flow_local)
+    t_flow_sk = sum(sk.result.phase_times.flow for sk, _ in runs)
+    t_total = sum(sk.result.phase_times.total + sv.result.phase_times.total for sk, sv in runs)
+    tr = load_json("r02/flow_kernel_traffic_cfg4.json")
+    fpairs = lse + bary + svp
+    roof = {
+        "bound": "mufu/fp32 (co-limited; composite of SURVEY.md 8(d) per-sweep roofs)",
+        "kernel": ("flow_kernel<float,3,2> (chunked fp32 Sinkhorn flow, cross + self solves) + "
+                   "sv_sweep_kernel<float,3,2> (SVGD)" if world == 1 else
+                   "sharded lse sweeps (ot_solve_kernel SWEEP mode) + sv_sweep_kernel"),
+        "achieved": fpairs / t_flow / 1e9,
+        "peak": fpairs / t_roof / 1e9,
+        "unit": "Gpair/s",
+        "frac": t_roof / t_flow,
+        "traffic": (tr["dram_bytes_per_launch"] if tr else None),
+        "traffic_source": (tr["source"] if tr else None),
+        "algorithmic_bytes_per_launch": (tr["algorithmic_bytes_per_launch"] if tr else None),
+        "pairs": {"lse_only": lse, "barycentre_and_self": bary, "svgd": svp},
+        "roofs_Gpair_s": {"lse": roof_lse / 1e9, "bary_svgd": roof_bary / 1e9},
+        "peaks_measured": {"mufu_ex2_Gops": peak["ex2"] / 1e9, "ffma_Gops": peak["ffma"] / 1e9,
+                           "source": "fcb_peak_probe in this run"},
+        "sinkhorn_flow_Gpair_s": (lse + bary) / max(t_flow_sk, 1e-12) / 1e9,
+        "sinkhorn_flow_frac_of_mufu": (lse + bary) / max(t_flow_sk, 1e-12) / peak["ex2"],
+        "ms_flow_per_step": t_flow / args.steps * 1e3,
+        "share_of_step": t_flow_local / max(t_total, 1e-12),
+        "launches_flow": int(sum(sk.result.iterations_used + sv.result.iterations_used
+                                 for sk, sv in runs)),
+    }
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.cpu_iterations)
+    secondary = None
+    if rank == 0 and world == 1:
+        if not args.no_secondary:
+            secondary = config2_secondary(torch, fc, _dev, lib, peak, min(args.steps, 10), flush)
+        if not args.no_cpu:
+            sk0 = runs[0][0]
+            cpu = cpu_baseline(sk0, pairs / args.steps)
 
     if rank == 0:
-        clk = clocks.summary()
         line = {
             "metric": METRIC,
-            "value": pairs_all / t_max,
+            "value": pairs / t_max,
             "unit": UNIT,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "fp32 pairwise sweeps (MUFU ex2), fp64 potentials/LQR/rollout",
-            "data": "synthetic: benchmark_mixture(2) draws, seed stream [rank, 2]",
+            "data": "synthetic: benchmark_mixture(3) draws (seed stream [0, 2]), "
+                    "random-small initial controls (stream [0, 1])",
             "config": {
-                "workload": WORKLOAD,
-                "T": T_STEPS, "M": M_TARGETS, "outer_iterations": ITERATIONS, "eta": ETA,
-                "problems": world, "parallelism": f"independent problems x{world}",
+                "workload": WORKLOAD, "T": T4, "M": M4, "d": D4,
+                "sinkhorn_iterations": SK_ITERS, "svgd_iterations": SV_ITERS,
+                "eta_sinkhorn": ETA_SK, "eta_svgd": ETA_SV, "svgd_bandwidth": H_SV,
+                "parallelism": ("single GPU" if world == 1 else
+                                f"M-sharded Sinkhorn + source-sharded SVGD over {world} GPUs"),
                 "l2": "256 MiB memset between steps (inputs < L2)",
             },
-            "planner_iters_per_s": iters_all / t_max,
-            "pairs_per_step": pairs_all / args.steps / world,
-            "e2e": {"value": e2e_pairs_all / t_e2e, "unit": UNIT,
-                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": t_e2e / args.steps * 1e3},
+            "planner_iters_per_s": iters / t_max,
+            "pairs_per_step": pairs / args.steps,
+            "e2e": {"value": e2e_pairs / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e / args.steps * 1e3},
             "gpu_launches": int(launches),
             "roofline": roof,
             "cpu_baseline": cpu,
-            "clocks": clk,
+            "secondary": secondary,
+            "clocks": clocks.summary(),
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def config2_secondary(torch, fc, _dev, lib, peak, steps, flush):
+    """BASELINE configs[1] on one GPU: the round-1 headline, for continuity."""
+    model = fc.double_integrator_2d()
+    Y = fc.benchmark_mixture(2).sample(M2, [0, 2])
+    disc = fc.Discretization(DT, T2, S0_DI)
+    cfg = fc.PlanConfig(method="sinkhorn", eta=ETA2, max_iterations=IT2, convergence_tol=0.0,
+                        metric_interval=0, seed=0)
+    q = fc.SamplePoints(Y)
+    Yd = _dev.f64(Y)
+    for _ in range(3):
+        fc.plan_detailed(model, q, disc, cfg, resident_targets=Yd)
+    torch.cuda.synchronize()
+    runs = []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        flush.zero_()
+        runs.append(fc.plan_detailed(model, q, disc, cfg, resident_targets=Yd))
+    e1 = torch.cuda.Event(enable_timing=True)
+    e1.record()
+    e1.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    pairs = sum(r.pairs for r in runs)
+    t_flow = sum(r.result.phase_times.flow for r in runs)
+    return {"workload": "BASELINE configs[1]: 2D double integrator, Sinkhorn, T=2000, M=1e4, "
+                        "200 iterations (persistent rs_plan_kernel)",
+            "value": pairs / t, "unit": UNIT, "steps": steps, "ms_per_step": t / steps * 1e3,
+            "planner_iters_per_s": sum(r.result.iterations_used for r in runs) / t,
+            "flow_phase_frac_of_mufu": pairs / t_flow / peak["ex2"],
+            "flow_share_of_step": t_flow / t}
+
+
 # ---------------------------------------------------------------------------
-# CPU (reference port) arm
+# CPU (reference port): a bounded sample of the config-4 step
 # ---------------------------------------------------------------------------
-def cpu_sample(outer: int, workers: int, seed: int = 0) -> tuple[float, float, float]:
-    """First `outer` iterations of the workload on the oracle port; (seconds, pairs, iters)."""
+def cpu_sample(workers: int, X0=None):
+    """One inner Sinkhorn iteration (g-sweep of all M samples over CPU_ROWS
+    trajectory points, f-sweep of those rows over all M) and one fixed-h SVGD
+    flow on CPU_SV points, on the oracle port.  Returns (seconds, pairs)."""
     from oracle import flowcover_oracle as O
 
-    Y = targets_for(seed)
+    Y = targets4()
+    q = O.benchmark_mixture(D4)
+    if X0 is None:
+        X0 = q.sample(CPU_ROWS, [5, 3])
+    X = X0[:CPU_ROWS]
+    Xs = q.sample(CPU_SV, [6, 3])
+    w = O.resolve_omega("auto", X, Y)
+    f = np.zeros(X.shape[0])
     t0 = time.perf_counter()
-    r = O.plan("double_integrator_2d", S0, DT, T_STEPS, "sinkhorn", ETA, outer, targets=Y,
-               seed=seed, workers=workers)
+    Lg = O.lse_sweep(Y, X, f, w, workers=workers)
+    g = w * (-np.log(Y.shape[0]) - Lg)
+    O.lse_sweep(X, Y, g, w, workers=workers)
+    O.stein_flow(Xs, q, H_SV, workers=workers)
     dt = time.perf_counter() - t0
-    pairs = sum(2.0 * ka * T_STEPS * M_TARGETS + ks * T_STEPS * T_STEPS for ka, ks in r["inner"])
-    return dt, pairs, float(len(r["flow_norms"]))
+    return dt, 2.0 * X.shape[0] * Y.shape[0] + float(CPU_SV) ** 2
 
 
-def cpu_baseline(outer: int) -> dict:
+def cpu_baseline(sk_run, pairs_per_step) -> dict:
     workers = os.cpu_count() or 1
-    dt, pairs, iters = cpu_sample(outer, workers)
-    return {"value": pairs / dt, "unit": UNIT, "cores": workers, "kind": "port",
-            "sample": f"first {outer} outer iterations of the workload (numpy float64 oracle, "
-                      f"{workers} threads)", "seconds": dt,
-            "planner_iters_per_s": iters / dt}
+    X0 = sk_run.result.trajectory.S[1:, :3]
+    cpu_sample(workers, X0)  # warm (imports, page-in)
+    dt, pairs = cpu_sample(workers, X0)
+    rate = pairs / dt
+    return {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": (f"one inner Sinkhorn iteration of {CPU_ROWS} trajectory rows x M=1e6 "
+                       f"(g- and f-sweep) + one SVGD flow on {CPU_SV} points, numpy float64 "
+                       f"oracle, {workers} threads"),
+            "seconds": dt,
+            "extrapolated_seconds_per_step": pairs_per_step / rate,
+            "extrapolated": True}
 
 
 def run_reference(args):
@@ -351,15 +429,13 @@ def run_reference(args):
     if rank != 0:
         return
     workers = os.cpu_count() or 1
-    outer = args.ref_outer
     for _ in range(args.warmup):
-        cpu_sample(1, workers)
-    tot_t = tot_p = tot_i = 0.0
+        cpu_sample(workers)
+    tot_t = tot_p = 0.0
     for _ in range(args.steps):
-        dt, pairs, iters = cpu_sample(outer, workers)
+        dt, pairs = cpu_sample(workers)
         tot_t += dt
         tot_p += pairs
-        tot_i += iters
     v = tot_p / tot_t
     line = {
         "impl": "reference",
@@ -371,19 +447,32 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": tot_t / args.steps * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic: benchmark_mixture(2) draws, seed stream [0, 2]",
-        "config": {"workload": WORKLOAD, "T": T_STEPS, "M": M_TARGETS,
-                   "sample_per_step": f"{outer} outer iterations"},
-        "planner_iters_per_s": tot_i / tot_t,
+        "data": "synthetic: benchmark_mixture(3) draws (seed stream [0, 2])",
+        "config": {"workload": WORKLOAD, "T": T4, "M": M4, "d": D4,
+                   "sample_per_step": (f"one inner Sinkhorn iteration on {CPU_ROWS} rows x "
+                                       f"M=1e6 + one SVGD flow on {CPU_SV} points")},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"{outer} outer iterations per step, oracle port of the "
-                                   f"reference (numpy float64, {workers} threads)"},
+                         "sample": "as config.sample_per_step; numpy float64 oracle port of "
+                                   f"the reference, {workers} threads"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
+
+
+def self_launch(args) -> int:
+    """--gpus N without torchrun: start N ranks (one per GPU) and relay rank 0."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -392,12 +481,16 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-iterations", type=int, default=6)
-    ap.add_argument("--ref-outer", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    _, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -266,6 +266,86 @@ FCB_API int fcb_plan_fused(int model, int ns, int m, const double* model_params,
                    int batch, const void* upd_ws, void* ws, size_t ws_bytes,
                    fcb_stream_t stream);
 
+/* ---- M-sharded flows (one process per GPU; distributed.py) ---------------
+ * Replaces the row-chunked thread pool of parallel.py:47-66 (used by
+ * sinkhorn.py:151-167 and stein.py:110-121) with a split of the reference
+ * samples (Sinkhorn) or the SVGD sources across GPUs.  These are the device
+ * steps; the caller runs the NCCL collectives between them on the same stream
+ * (csrc/shard.cu has the schedule).  ctl: device int[8] loop-control words,
+ * eslot: device unsigned long long[2]; both owned by the caller and reset by
+ * fcb_shard_init.  Kernels of a finished solve are no-ops. */
+
+/* out = {sum of coordinates (d), sum |p|^2, n}: the per-shard statistics of
+ * resolve_omega (sinkhorn.py:136-148), summed over ranks by the caller. */
+FCB_API int fcb_point_sums(const double* P, int n, int d, double* out, fcb_stream_t stream);
+
+/* One _lse_rows sweep (sinkhorn.py:151-167) of rows R (nr) against columns S
+ * (ns) with column potential pot: L_i = LSE_j((pot_j - |r_i - s_j|^2)/omega).
+ * out (nullable) = out_scale omega (out_shift - L) when out_scale != 0, else
+ * L (omega = scal[0]: the g-update w (log b - L) is out_scale 1, shift log b);
+ * bary (nullable, nr*(d+1)) = {L_i, softmax-weighted mean of the columns}. */
+FCB_API size_t fcb_lse_sweep_workspace_bytes(int precision, int nr, int ns, int d);
+FCB_API int fcb_lse_sweep(int precision, const double* R, int nr, const double* S, int ns, int d,
+                          const double* scal, const double* pot, double out_scale,
+                          double out_shift, double* out, double* bary, const int* gate, void* ws,
+                          size_t ws_bytes, fcb_stream_t stream);
+
+/* Flow start: omega from X and the global Y sums ysum (d+2), both centrings
+ * (scal_x: cross solve, scal_s: self solve; resolve_omega layout), f/p from
+ * the warm state or zero, ctl/eslot reset.  plan_state != 0 skips the flow. */
+FCB_API int fcb_shard_init(int precision, const double* X, int n, int d, const double* ysum,
+                           double omega_fixed, const double* warm_f, const double* warm_p,
+                           const int* warm_valid, double* scal_x, double* scal_s, double* f,
+                           double* p, int* ctl, unsigned long long* eslot, const int* plan_state,
+                           fcb_stream_t stream);
+
+/* Cross solve f-update (sinkhorn.py:190-205) from the gathered shard partials
+ * gathered[R][n][d+1] = {L_r, barycentre_r}: fixed-order LSE merge, f_new,
+ * err, row sums / plan mass / barycentres of the current f, stop decision
+ * (stat = {err, iters, converged, 0}); f <- f_new unless stopped. */
+FCB_API int fcb_shard_cross_merge(int n, int d, int R, const double* gathered, const double* scal,
+                                  double tol, int max_iters, double* f, double* fnext, double* rs,
+                                  double* mass, double* ybar, int* ctl, unsigned long long* eslot,
+                                  double* stat, fcb_stream_t stream);
+
+/* Self solve (sinkhorn.py:208-236), rows [row0, row0+nown) of X: Lb from
+ * fcb_lse_sweep (bary form) -> send[nown][d+4] = {p_new, rho, mass, err_i, xbar}. */
+FCB_API int fcb_shard_self_rows(int n, int d, int row0, int nown, const double* Lb,
+                                const double* scal, const double* p, double* send, const int* ctl,
+                                fcb_stream_t stream);
+/* gathered[R][chunk][d+4] (balanced contiguous shards) -> p_new, rho, mass,
+ * xbar for all rows, err and the stop decision; p <- p_new unless stopped. */
+FCB_API int fcb_shard_self_commit(int n, int d, int R, int chunk, const double* gathered,
+                                  double tol, int max_iters, double* p, double* pnext, double* rho,
+                                  double* massp, double* xbar, int* ctl, unsigned long long* eslot,
+                                  double* stat, fcb_stream_t stream);
+
+/* Envelope gradient (sinkhorn.py:383-391), FlowError test (:370-373), warm
+ * state (:393-395) and the planner hooks of fcb_sinkhorn_flow. */
+FCB_API size_t fcb_shard_finish_workspace_bytes(int n);
+FCB_API int fcb_shard_flow_finish(const double* X, int n, int d, const double* rs,
+                                  const double* mass, const double* ybar, const double* rho,
+                                  const double* massp, const double* xbar, const double* stat_x,
+                                  const double* stat_p, double tol, const double* f,
+                                  const double* p, double* warm_f, double* warm_p, int* warm_valid,
+                                  double* flow, double* fstat, const double* scal, int* plan_state,
+                                  int iteration, double* flow_log, double conv_tol, int* ctl,
+                                  void* ws, size_t ws_bytes, fcb_stream_t stream);
+
+/* SVGD (stein.py:79-122) over the source points [col0, col0+ncols) for all n
+ * queries: part[n][d+1] = {sum_j k_ij, sum_j k_ij (s_j - (2/h) x'_j)} with x'
+ * centred on X[0].  fcb_stein_combine sums R such partials in rank order,
+ * writes the flow and runs the planner hooks of fcb_stein_flow_full. */
+FCB_API size_t fcb_stein_partial_workspace_bytes(int precision, int n, int nc, int d);
+FCB_API int fcb_stein_partial(int precision, const double* X, int n, int d, int col0, int ncols,
+                              const double* scores, const double* hstat, double* part,
+                              const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream);
+FCB_API size_t fcb_stein_combine_workspace_bytes(int n);
+FCB_API int fcb_stein_combine(const double* X, int n, int d, int R, const double* parts,
+                              const double* hstat, double* flow, double* fstat, int* plan_state,
+                              int iteration, double* flow_log, double conv_tol, void* ws,
+                              size_t ws_bytes, fcb_stream_t stream);
+
 /* ---- measurement helpers ------------------------------------------------- */
 
 /* MUFU.EX2 / FFMA throughput probe used by bench.py for the roofline

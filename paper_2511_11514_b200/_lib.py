@@ -103,6 +103,25 @@ SIGNATURES: dict[str, tuple] = {
         [_I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _P, _D, _P, _P, _I, _D,
          _I, _D, _D, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _Z, _P],
     ),
+    "fcb_point_sums": (_I, [_P, _I, _I, _P, _P]),
+    "fcb_lse_sweep_workspace_bytes": (_Z, [_I, _I, _I, _I]),
+    "fcb_lse_sweep": (_I, [_I, _P, _I, _P, _I, _I, _P, _P, _D, _D, _P, _P, _P, _P, _Z, _P]),
+    "fcb_shard_init": (_I, [_I, _P, _I, _I, _P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "fcb_shard_cross_merge": (
+        _I, [_I, _I, _I, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "fcb_shard_self_rows": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "fcb_shard_self_commit": (
+        _I, [_I, _I, _I, _I, _P, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "fcb_shard_finish_workspace_bytes": (_Z, [_I]),
+    "fcb_shard_flow_finish": (
+        _I,
+        [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I,
+         _P, _D, _P, _P, _Z, _P],
+    ),
+    "fcb_stein_partial_workspace_bytes": (_Z, [_I, _I, _I, _I]),
+    "fcb_stein_partial": (_I, [_I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _Z, _P]),
+    "fcb_stein_combine_workspace_bytes": (_Z, [_I]),
+    "fcb_stein_combine": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _D, _P, _Z, _P]),
     "fcb_peak_probe": (_I, [_I, _I, _P, _P]),
     "fcb_debug_timeline": (_I, [_P, _I]),
 }

@@ -5,10 +5,11 @@
 //   backward: e_k     = M_k e_{k+1} + c_k (e_T given)      k = T-1..0
 //
 // Three launches, no grid-wide synchronisation:
-//   K1  every CTA owns AS_BLK consecutive steps; each thread builds its step
-//       map (all per-step loads in flight at once), then a Hillis-Steele scan
-//       in shared memory composes the block's maps; the block aggregate goes
-//       to global memory.
+//   K1  every CTA owns AS_BLK consecutive chunks of CH steps (CH = 1 up to
+//       AS_BLK * 148 steps, more for longer horizons so K2 sees ~148
+//       aggregates); each thread composes its chunk's step maps, then a
+//       Hillis-Steele scan in shared memory composes the block's maps; the
+//       block aggregate goes to global memory.
 //   K2  one CTA scans the block aggregates and writes the state entering each
 //       block.
 //   K3  every CTA repeats its in-block scan, applies it to its entry state and
@@ -23,6 +24,7 @@
 namespace fcb {
 
 constexpr int AS_BLK = 128;
+constexpr int AS_K2 = 256;  // threads of the aggregate scan (few registers spill at 256)
 
 template <int N>
 struct AMap {
@@ -95,13 +97,38 @@ constexpr int amap_doubles() {
 // In-block inclusive scan (prefix for FWD, suffix for BWD) of the maps of
 // steps blockIdx.x*AS_BLK + t; returns this thread's inclusive map.  buf:
 // shared memory of 2*AS_BLK*amap_doubles<N>() doubles.
+// Steps per thread chunk of the three-launch scan.
+__host__ __device__ __forceinline__ int affscan_chunk(int T) {
+    const int per = AS_BLK * 148;
+    return T > per ? (T + per - 1) / per : 1;
+}
+
+// The map of one thread's chunk [k0, k0 + CH) (clipped at T): later o earlier.
+template <int N, bool FWD, class MapFn>
+__device__ __forceinline__ void chunk_map(const MapFn& mapf, int T, int k0, int CH, AMap<N>& mine) {
+    if (CH == 1) {
+        if (k0 < T) mapf(k0, mine);
+        else amap_identity<N>(mine);
+        return;
+    }
+    amap_identity<N>(mine);
+    for (int j = 0; j < CH; ++j) {
+        // FWD applies steps in increasing k, BWD in decreasing k
+        const int k = FWD ? k0 + j : k0 + CH - 1 - j;
+        if (k >= T) continue;
+        AMap<N> step, res;
+        mapf(k, step);
+        amap_compose<N>(step, mine, res);
+        mine = res;
+    }
+}
+
 template <int N, bool FWD, class MapFn>
 __device__ __forceinline__ void block_scan(const MapFn& mapf, int T, double* buf, AMap<N>& mine) {
     constexpr int AD = amap_doubles<N>();
     const int t = threadIdx.x;
-    const int k = blockIdx.x * AS_BLK + t;
-    if (k < T) mapf(k, mine);
-    else amap_identity<N>(mine);
+    const int CH = affscan_chunk(T);
+    chunk_map<N, FWD, MapFn>(mapf, T, (blockIdx.x * AS_BLK + t) * CH, CH, mine);
     double* cur = buf;
     double* nxt = buf + AS_BLK * AD;
     amap_copy_to<N>(cur + t * AD, mine);
@@ -138,18 +165,17 @@ __global__ void __launch_bounds__(AS_BLK) affscan_k1(int T, MapFn mapf, double* 
 // One CTA: entry state of every block.  FWD: entry(b) = Agg_{b-1} o ... o
 // Agg_0 (s0).  BWD: entry(b) = Agg_{b+1} o ... o Agg_{nb-1} (eT), i.e. the
 // state after the block's last step.  Hillis-Steele over the aggregates in
-// global ping-pong buffers (nb <= 1024 blocks, T <= 131072 steps).
+// global ping-pong buffers (nb ~ 148 for long horizons: see affscan_chunk).
 template <int N, bool FWD>
-__global__ void __launch_bounds__(1024) affscan_k2(int nb, const double* __restrict__ init,
+__global__ void __launch_bounds__(AS_K2) affscan_k2(int nb, const double* __restrict__ init,
                                                    double* __restrict__ agg, double* __restrict__ tmp,
                                                    double* __restrict__ entry, const int* gate) {
     constexpr int AD = amap_doubles<N>();
     if (gate && *((volatile const int*)gate) != 0) return;
-    const int t = threadIdx.x;
     double* cur = agg;
     double* nxt = tmp;
     for (int s = 1; s < nb; s <<= 1) {
-        if (t < nb) {
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) {
             AMap<N> mine, other, res;
             amap_copy_from<N>(cur + (size_t)t * AD, mine);
             const int o = FWD ? t - s : t + s;
@@ -165,7 +191,7 @@ __global__ void __launch_bounds__(1024) affscan_k2(int nb, const double* __restr
         cur = nxt;
         nxt = x;
     }
-    if (t < nb) {
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
         double x0[N], y[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) x0[i] = init ? init[i] : 0.0;
@@ -200,12 +226,12 @@ __global__ void __launch_bounds__(AS_BLK) affscan_k3(int T, MapFn mapf, OutFn ou
     // map; the exclusive map of thread t is the inclusive one of t-1 (FWD) or
     // t+1 (BWD), identity at the block edge
     const int t = threadIdx.x;
-    const int k = blockIdx.x * AS_BLK + t;
+    const int CH = affscan_chunk(T);
+    const int k0 = (blockIdx.x * AS_BLK + t) * CH;
     const double* fin = sbuf + ((31 - __clz(AS_BLK)) % 2 == 0 ? 0 : AS_BLK * AD);
     double ein[N], before[N], after[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) ein[i] = entry[(size_t)blockIdx.x * N + i];
-    amap_apply<N>(mine, ein, after);
     const int o = FWD ? t - 1 : t + 1;
     if (o >= 0 && o < AS_BLK) {
         AMap<N> ex;
@@ -216,7 +242,22 @@ __global__ void __launch_bounds__(AS_BLK) affscan_k3(int T, MapFn mapf, OutFn ou
         for (int i = 0; i < N; ++i) before[i] = ein[i];
     }
     double v = 0.0;
-    if (k < T) v = out(k, before, after);
+    if (CH == 1) {
+        amap_apply<N>(mine, ein, after);
+        if (k0 < T) v = out(k0, before, after);
+    } else {
+        // re-walk the chunk from the state entering it (FWD: s_k0; BWD: e_{k0+CH})
+        for (int j = 0; j < CH; ++j) {
+            const int k = FWD ? k0 + j : k0 + CH - 1 - j;
+            if (k >= T) continue;
+            AMap<N> step;
+            mapf(k, step);
+            amap_apply<N>(step, before, after);
+            v += out(k, before, after);
+#pragma unroll
+            for (int i = 0; i < N; ++i) before[i] = after[i];
+        }
+    }
     v = warp_sum(v);
     if ((t & 31) == 0) s_red[t >> 5] = v;
     __syncthreads();
@@ -232,7 +273,10 @@ inline size_t affscan_smem_bytes() {
     return 2 * AS_BLK * amap_doubles<N>() * sizeof(double);
 }
 
-inline int affscan_blocks(int T) { return (T + AS_BLK - 1) / AS_BLK; }
+inline int affscan_blocks(int T) {
+    const int steps = AS_BLK * affscan_chunk(T);
+    return (T + steps - 1) / steps;
+}
 
 // scratch doubles: aggregates (2 x nb maps), entries (nb x N), block sums (nb)
 template <int N>
@@ -275,7 +319,7 @@ inline int affscan_run(int T, const MapFn& mapf, const OutFn& out, const double*
         attr = true;
     }
     affscan_k1<N, FWD, MapFn><<<nb, AS_BLK, smem, st>>>(T, mapf, b.agg, gate);
-    affscan_k2<N, FWD><<<1, 1024, 0, st>>>(nb, init, b.agg, b.tmp, b.entry, gate);
+    affscan_k2<N, FWD><<<1, AS_K2, 0, st>>>(nb, init, b.agg, b.tmp, b.entry, gate);
     affscan_k3<N, FWD, MapFn, OutFn><<<nb, AS_BLK, smem, st>>>(T, mapf, out, b.entry, b.red, gate);
     return 3;
 }
@@ -400,7 +444,9 @@ __device__ __forceinline__ void wait_flag(const unsigned* flags, int t, unsigned
 
 constexpr int FUSED_MAX_BLOCKS = AS_BLK;
 
-inline bool fused_scan_ok(int T) { return T >= 1 && affscan_blocks(T) <= FUSED_MAX_BLOCKS; }
+// The one-launch scans take one step per thread.
+inline int fused_blocks(int T) { return (T + AS_BLK - 1) / AS_BLK; }
+inline bool fused_scan_ok(int T) { return T >= 1 && fused_blocks(T) <= FUSED_MAX_BLOCKS; }
 
 // Workspace of fused scans: per slot nb aggregates and nb flags.
 template <int N>

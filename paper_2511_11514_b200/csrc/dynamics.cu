@@ -317,19 +317,19 @@ struct LiftedFlow {
 };
 
 // The Riccati phase (lqr_split.cuh) as three launches over the whole GPU:
-// chunk aggregates + in-CTA suffix scan, the suffix scan over CTAs, and the
-// per-step re-walk emitting the gains.  The plan_* variants evaluate the
+// warp chunk aggregates + in-CTA suffix scan, the suffix scan over CTAs, and
+// the per-step re-walk emitting the gains.  The plan_* variants evaluate the
 // model's Jacobians along (S, U) on the fly and are gated by the planner
 // status word.
 template <int N, int M>
-__global__ void __launch_bounds__(RIC_BLOCK) ric_arrays_k1(RicArgs p, const double* A,
-                                                           const double* B) {
+__global__ void __launch_bounds__(RW_BLOCK) ric_arrays_k1(RicArgs p, const double* A,
+                                                          const double* B) {
     ArrayJac<N, M> jac{A, B};
     riccati_k1<N, M>(jac, p);
 }
 template <int N, int M>
-__global__ void __launch_bounds__(RIC_BLOCK) ric_arrays_k3(RicArgs p, const double* A,
-                                                           const double* B) {
+__global__ void __launch_bounds__(RW_BLOCK) ric_arrays_k3(RicArgs p, const double* A,
+                                                          const double* B) {
     ArrayJac<N, M> jac{A, B};
     riccati_k3<N, M>(jac, p);
 }
@@ -339,26 +339,24 @@ __device__ __forceinline__ bool ric_gated(const RicArgs& p) {
 }
 
 template <class Mdl>
-__global__ void __launch_bounds__(RIC_BLOCK) plan_ric_k1(RicArgs p, const double* prm,
-                                                         const double* S, const double* U) {
+__global__ void __launch_bounds__(RW_BLOCK) plan_ric_k1(RicArgs p, const double* prm,
+                                                        const double* S, const double* U) {
     if (ric_gated(p)) return;
     ModelJac<Mdl> jac{prm, S, U};
     riccati_k1<Mdl::N, Mdl::M>(jac, p);
 }
 template <class Mdl>
-__global__ void __launch_bounds__(RIC_BLOCK) plan_ric_k3(RicArgs p, const double* prm,
-                                                         const double* S, const double* U) {
+__global__ void __launch_bounds__(RW_BLOCK) plan_ric_k3(RicArgs p, const double* prm,
+                                                        const double* S, const double* U) {
     if (ric_gated(p)) return;
     ModelJac<Mdl> jac{prm, S, U};
     riccati_k3<Mdl::N, Mdl::M>(jac, p);
 }
 
-constexpr int RIC_K2_THREADS = 512;
-
-template <int N>
-__global__ void __launch_bounds__(RIC_K2_THREADS) ric_k2(RicArgs p) {
+template <int N, int M>
+__global__ void __launch_bounds__(32 * RW_K2_WARPS) ric_k2(RicArgs p) {
     if (ric_gated(p)) return;
-    riccati_k2<N>(p);
+    riccati_k2<N, M>(p);
 }
 
 __global__ void ric_finish_kernel(RicArgs p) {
@@ -366,7 +364,25 @@ __global__ void ric_finish_kernel(RicArgs p) {
     riccati_finish(p);
 }
 
-static int ric_max_blocks() { return std::min(2 * sm_count(), RIC_K2_THREADS); }
+// Launch one Riccati kernel with its dynamic shared memory (opt-in > 48 KB).
+template <typename... Args>
+static void ric_launch(void (*kern)(Args...), int grid, int warps, size_t smem, cudaStream_t st,
+                       Args... args) {
+    cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 32 * warps, smem, st>>>(args...);
+}
+
+// Riccati phase on explicit or model Jacobians: K1, K2, K3 (+ finish).
+template <int N, int M, class K1, class K3, typename... J>
+static int ric_phase(K1 k1, K3 k3, const RicArgs& r, cudaStream_t st, bool finish, J... jargs) {
+    ric_launch(k1, r.nblk, RW_WARPS, rw_smem_bytes<N, M>(RW_WARPS), st, r, jargs...);
+    ric_launch(ric_k2<N, M>, 1, RW_K2_WARPS, rw_smem_bytes<N, M>(RW_K2_WARPS), st, r);
+    ric_launch(k3, r.nblk, RW_WARPS, rw_smem_bytes<N, M>(RW_WARPS), st, r, jargs...);
+    if (finish) ric_finish_kernel<<<1, 32, 0, st>>>(r);
+    return finish ? 4 : 3;
+}
+
+static int ric_max_blocks() { return sm_count(); }
 
 // ---------------------------------------------------------------------------
 // dispatch
@@ -610,7 +626,7 @@ static int launch_rollout(int method, const double* prm, const double* s0, const
             RollWs L = roll_layout(N, T, ws);
             auto kern = roll_fused_linear_kernel<Mdl>;
             const size_t smem = fused_smem(kern, fused_smem_bytes<N>());
-            kern<<<affscan_blocks(T), AS_BLK, smem, st>>>(prm, dt, s0, U, T, S, d, P, X, status,
+            kern<<<fused_blocks(T), AS_BLK, smem, st>>>(prm, dt, s0, U, T, S, d, P, X, status,
                                                           plan_state, iteration, L.fw,
                                                           next_scan_tag());
             return 1;
@@ -633,7 +649,7 @@ static int launch_rollout(int method, const double* prm, const double* s0, const
             auto kern = roll_fused_tri_kernel<Mdl>;
             constexpr int NMAX = Mdl::NQ > Mdl::NP ? Mdl::NQ : Mdl::NP;
             const size_t smem = fused_smem(kern, fused_smem_bytes<NMAX>());
-            kern<<<affscan_blocks(T), AS_BLK, smem, st>>>(s0, U, T, dt, S, d, P, X, L.dp, status,
+            kern<<<fused_blocks(T), AS_BLK, smem, st>>>(s0, U, T, dt, S, d, P, X, L.dp, status,
                                                           plan_state, iteration, L.fw,
                                                           next_scan_tag());
             return 1;
@@ -698,7 +714,7 @@ static LqrWs lqr_layout(int ns, int m, int T, void* ws) {
     Arena ar(ws, ws ? (size_t)-1 : 0);
     LqrWs L{};
     L.geom = ric_geom(T, ric_max_blocks());
-    L.agg = ar.take<double>(2 * (size_t)L.geom.nthr * 3 * ns * ns);
+    L.agg = ar.take<double>(2 * (size_t)L.geom.nwarp * 3 * ns * ns);
     L.bagg = ar.take<double>(2 * (size_t)L.geom.nblk * 3 * ns * ns);
     L.K = ar.take<double>((size_t)T * m * ns);
     L.Lg = ar.take<double>((size_t)T * m * ns);
@@ -723,7 +739,7 @@ static RicArgs ric_args(const LqrWs& L, int T, double dt, const double* Q, const
     r.agg = L.agg;
     r.bagg = L.bagg;
     r.L = L.geom.L;
-    r.nthr = L.geom.nthr;
+    r.nwarp = L.geom.nwarp;
     r.nblk = L.geom.nblk;
     r.K = L.K;
     r.Lg = L.Lg;
@@ -748,7 +764,7 @@ static int affine_phase(const LqrWs& L, const double* K, double* dff, int T, dou
     if (fused_scan_ok(T)) {
         auto kern = affine_fused_kernel<N, M, Flow>;
         const size_t smem = fused_smem(kern, fused_smem_bytes<N>());
-        kern<<<affscan_blocks(T), AS_BLK, smem, st>>>(T, emap, eout, zmap, zout, L.fw,
+        kern<<<fused_blocks(T), AS_BLK, smem, st>>>(T, emap, eout, zmap, zout, L.fw,
                                                       next_scan_tag(), L.fail, reset_fail, cost,
                                                       lqr_costs, plan_state, iteration);
         return 1;
@@ -778,11 +794,9 @@ static int lqr_solve_t(int T, double dt, const double* A, const double* B, const
                        const double* R, const double* a, double* v, double* z, double* K,
                        double* dff, double* scal, const LqrWs& L, cudaStream_t st) {
     RicArgs r = ric_args(L, T, dt, Q, R);
-    ric_arrays_k1<N, M><<<r.nblk, RIC_BLOCK, 0, st>>>(r, A, B);
-    ric_k2<N><<<1, RIC_K2_THREADS, 0, st>>>(r);
-    ric_arrays_k3<N, M><<<r.nblk, RIC_BLOCK, 0, st>>>(r, A, B);
+    const int nr = ric_phase<N, M>(ric_arrays_k1<N, M>, ric_arrays_k3<N, M>, r, st, false, A, B);
     ArrayFlow<N> fl{a};
-    int n = 3 + affine_phase<N, M>(L, L.K, dff ? dff : L.dff, T, dt, Q, R, fl, v, z, nullptr,
+    int n = nr + affine_phase<N, M>(L, L.K, dff ? dff : L.dff, T, dt, Q, R, fl, v, z, nullptr,
                                    nullptr, 0.0, nullptr, scal, nullptr, nullptr, 0, 0, st);
     if (K) {  // gains to the caller's step-major layout [T][M][N]
         const int blocks = std::min(4 * sm_count(), (T * M * N + 255) / 256);
@@ -833,11 +847,7 @@ static int launch_plan_update(int mode, const LqrWs& L, int T, double dt, const 
         RicArgs r = ric_args(L, T, dt, Q, R);
         r.plan_state = plan_state;
         r.iteration = iteration;
-        plan_ric_k1<Mdl><<<r.nblk, RIC_BLOCK, 0, st>>>(r, prm, S, U);
-        ric_k2<N><<<1, RIC_K2_THREADS, 0, st>>>(r);
-        plan_ric_k3<Mdl><<<r.nblk, RIC_BLOCK, 0, st>>>(r, prm, S, U);
-        ric_finish_kernel<<<1, 32, 0, st>>>(r);
-        n = 4;
+        n = ric_phase<N, M>(plan_ric_k1<Mdl>, plan_ric_k3<Mdl>, r, st, true, prm, S, U);
     }
     // mode 1: fail := -1, the stored Riccati phase is valid
     LiftedFlow<N> fl{flow, P, d};

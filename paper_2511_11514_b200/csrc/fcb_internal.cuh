@@ -77,6 +77,10 @@ struct Arena {
 // device helpers
 // ---------------------------------------------------------------------------
 constexpr double kLog2e = 1.4426950408889634073599;
+
+// scal[] layout of a transport solve (device double[16]; fcb_resolve_omega)
+enum { SC_OMEGA = 0, SC_S = 1, SC_C = 2 /*2..4*/, SC_MX2 = 5, SC_MX = 6 /*6..8*/, SC_MY2 = 9,
+       SC_MY = 10 /*10..12*/ };
 constexpr double kLn2 = 0.6931471805599453094172;
 
 __device__ __forceinline__ float ex2_approx(float x) {

@@ -169,20 +169,36 @@ __device__ void lqr_shared_init(LqrShared<N, M>& s, const double* Q, const doubl
     __syncthreads();
 }
 
-// Riccati-phase launch geometry: RIC_BLOCK threads per CTA, each thread owns
-// a chunk of `L` consecutive elements (the zero terminal element T included).
-constexpr int RIC_BLOCK = 128;
-constexpr int RIC_MIN_CHUNK = 4;
+// ---------------------------------------------------------------------------
+// Riccati phase over the whole GPU, warp-cooperative.
+//
+// The (A, C, J) element of a 6-state model is 108 doubles; a thread-private
+// combine needs three of them live and spills to local memory, which at
+// 10^5 steps turns the scan into an HBM-bound local-memory stream.  Here one
+// WARP owns a chunk of consecutive elements and every element operation is
+// spread over its 32 lanes, with the operands in the warp's shared-memory
+// slice:
+//   K1  each warp folds its chunk into one aggregate (suffix order); the CTA
+//       runs a Hillis-Steele suffix scan over its warps' aggregates;
+//   K2  one CTA scans the CTA aggregates;
+//   K3  each warp forms J after its chunk (next warp's in-CTA suffix composed
+//       with the next CTAs' suffix) and re-walks the chunk in information form,
+//       emitting K_k, H_k^-1 G_k', Acl_k, G_k per step.
+// ---------------------------------------------------------------------------
+constexpr int RW_WARPS = 16;              // warps per CTA (K1, K3)
+constexpr int RW_BLOCK = 32 * RW_WARPS;
+constexpr int RW_K2_WARPS = 32;
+constexpr int RW_MIN_CHUNK = 8;
 
 struct RicArgs {
     int T;
     double dt;
     const double* Q;
     const double* R;
-    int L;        // elements per thread chunk
-    int nthr;     // threads with a chunk slot (nblk * RIC_BLOCK)
-    int nblk;     // CTAs of the thread-level kernels
-    double* agg;  // 2 * nthr * 3N^2: chunk aggregates -> in-CTA suffixes (ping-pong)
+    int L;        // elements per warp chunk
+    int nwarp;    // warps with a chunk slot (nblk * RW_WARPS)
+    int nblk;     // CTAs of K1 / K3
+    double* agg;  // 2 * nwarp * 3N^2: warp aggregates -> in-CTA suffixes (ping-pong)
     double* bagg; // 2 * nblk * 3N^2: CTA aggregates -> their suffix scan (ping-pong)
     // per-step outputs, element-major: X[e * T + k]
     double* K;    // M*N x T
@@ -202,322 +218,433 @@ __host__ __device__ __forceinline__ int hs_rounds(int n) {
     return r;
 }
 
-template <int N>
-__device__ __forceinline__ void elemr_identity(ElemR<N>& e) {
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-            e.A[i][j] = (i == j) ? 1.0 : 0.0;
-            e.C[i][j] = 0.0;
-            e.J[i][j] = 0.0;
-        }
+// Shared-memory slice of one warp.
+template <int N, int M>
+struct RwWarp {
+    double E[3][3 * N * N];  // element slots (A | C | J, row-major)
+    double Mt[N * N];
+    double W[N * 2 * N];
+    double Tm[N * N];
+    double JA[N * N];
+    double F[N * N];
+    double G[N * M];
+    double J2[N * N];
+    double PG[N * M];
+    double H[M * M];
+    double rhs[M * 2 * N];
+};
+
+template <int N, int M>
+constexpr size_t rw_smem_bytes(int warps) {
+    return sizeof(LqrShared<N, M>) + (size_t)warps * sizeof(RwWarp<N, M>);
 }
 
-// F = I + dt A_k, G = dt B_k at step k and the base element
-// e_k = (F, G Rt^-1 G', 2 Qb); the terminal element (k >= T) is zero.
+// In-place Gauss-Jordan elimination with partial pivoting by one warp:
+// Mt (n x n) X = W (n x r); on return W holds X.  n <= 6, r <= 12.
+template <int NN, int RR>
+__device__ __forceinline__ void warp_gauss_jordan(double* Mt, double* W, int lane) {
+    constexpr int C = NN + RR;
+    constexpr int TOT = NN * C;
+    constexpr int PER = (TOT + 31) / 32;
+    for (int col = 0; col < NN; ++col) {
+        int piv = col;
+        double best = fabs(Mt[col * NN + col]);
+        for (int r = col + 1; r < NN; ++r) {
+            const double v = fabs(Mt[r * NN + col]);
+            if (v > best) {
+                best = v;
+                piv = r;
+            }
+        }
+        if (piv != col) {
+            for (int c = lane; c < C; c += 32) {
+                double* a = c < NN ? &Mt[col * NN + c] : &W[col * RR + c - NN];
+                double* b = c < NN ? &Mt[piv * NN + c] : &W[piv * RR + c - NN];
+                const double t = *a;
+                *a = *b;
+                *b = t;
+            }
+            __syncwarp();
+        }
+        const double inv = 1.0 / Mt[col * NN + col];
+        double v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int idx = lane + 32 * k;
+            if (idx < TOT) {
+                const int r = idx / C, c = idx % C;
+                const double pr = (c < NN ? Mt[col * NN + c] : W[col * RR + c - NN]) * inv;
+                const double cur = c < NN ? Mt[r * NN + c] : W[r * RR + c - NN];
+                v[k] = (r == col) ? pr : cur - Mt[r * NN + col] * pr;
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int idx = lane + 32 * k;
+            if (idx < TOT) {
+                const int r = idx / C, c = idx % C;
+                if (c < NN) Mt[r * NN + c] = v[k];
+                else W[r * RR + c - NN] = v[k];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// out = e1 (x) e2 (e1 earlier in time) on (A, C, J), by one warp:
+//   X = (I + C1 J2)^-1 [A1 | C1],  A = A2 X_A,  C = A2 X_C A2' + C2,
+//   J = X_A' J2 A1 + J1  (then C, J symmetrised).
+template <int N, int M>
+__device__ void warp_combine(const double* e1, const double* e2, double* out, RwWarp<N, M>& w,
+                             int lane) {
+    constexpr int NN = N * N;
+    const double *A1 = e1, *C1 = e1 + NN, *J1 = e1 + 2 * NN;
+    const double *A2 = e2, *C2 = e2 + NN, *J2 = e2 + 2 * NN;
+    double *oA = out, *oC = out + NN, *oJ = out + 2 * NN;
+    for (int idx = lane; idx < NN; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) s += C1[i * N + q] * J2[q * N + j];
+        w.Mt[idx] = s;
+    }
+    for (int idx = lane; idx < 2 * NN; idx += 32) {
+        const int i = idx / (2 * N), j = idx % (2 * N);
+        w.W[idx] = j < N ? A1[i * N + j] : C1[i * N + j - N];
+    }
+    __syncwarp();
+    warp_gauss_jordan<N, 2 * N>(w.Mt, w.W, lane);
+    for (int idx = lane; idx < 2 * NN; idx += 32) {
+        const int i = idx / (2 * N), j = idx % (2 * N);
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) s += A2[i * N + q] * w.W[q * 2 * N + j];
+        if (j < N) oA[i * N + j] = s;
+        else w.Tm[i * N + j - N] = s;
+    }
+    for (int idx = lane; idx < NN; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) s += J2[i * N + q] * A1[q * N + j];
+        w.JA[idx] = s;
+    }
+    __syncwarp();
+    for (int idx = lane; idx < NN; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        double c = 0.0, t = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            c += w.Tm[i * N + q] * A2[j * N + q];
+            t += w.W[q * 2 * N + i] * w.JA[q * N + j];
+        }
+        oC[idx] = c + C2[idx];
+        oJ[idx] = t + J1[idx];
+    }
+    __syncwarp();
+    for (int idx = lane; idx < NN; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        if (i < j) {
+            const double c = 0.5 * (oC[i * N + j] + oC[j * N + i]);
+            const double t = 0.5 * (oJ[i * N + j] + oJ[j * N + i]);
+            oC[i * N + j] = c;
+            oC[j * N + i] = c;
+            oJ[i * N + j] = t;
+            oJ[j * N + i] = t;
+        }
+    }
+    __syncwarp();
+}
+
+// F = I + dt A_k, G = dt B_k into the warp slice (lane 0 evaluates the model).
 template <int N, int M, class Jac>
-struct RicSteps {
-    const Jac& jac;
-    const LqrShared<N, M>& sh;
-    int T;
-    double dt;
-    __device__ __forceinline__ void fg(int k, double (&F)[N][N], double (&G)[N][M]) const {
+__device__ __forceinline__ void warp_fg(const Jac& jac, int k, double dt, RwWarp<N, M>& w,
+                                        int lane) {
+    if (lane == 0) {
         double a[N * N], b[N * M];
         jac.get(k, a, b);
 #pragma unroll
         for (int i = 0; i < N; ++i) {
 #pragma unroll
-            for (int j = 0; j < N; ++j) F[i][j] = (i == j ? 1.0 : 0.0) + dt * a[i * N + j];
+            for (int j = 0; j < N; ++j) w.F[i * N + j] = (i == j ? 1.0 : 0.0) + dt * a[i * N + j];
 #pragma unroll
-            for (int j = 0; j < M; ++j) G[i][j] = dt * b[i * M + j];
+            for (int j = 0; j < M; ++j) w.G[i * M + j] = dt * b[i * M + j];
         }
     }
-    __device__ __forceinline__ void base(int k, ElemR<N>& e) const {
-        if (k >= T) {
-#pragma unroll
-            for (int i = 0; i < N; ++i)
-#pragma unroll
-                for (int j = 0; j < N; ++j) e.A[i][j] = e.C[i][j] = e.J[i][j] = 0.0;
-            return;
-        }
-        double F[N][N], G[N][M];
-        fg(k, F, G);
-        base_fg(F, G, e);
-    }
-    __device__ __forceinline__ void base_fg(const double (&F)[N][N], const double (&G)[N][M],
-                                            ElemR<N>& e) const {
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                e.A[i][j] = F[i][j];
-                e.J[i][j] = 2.0 * sh.Qb[i][j];
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < M; ++q) {
-                    double gr = 0.0;
-#pragma unroll
-                    for (int r = 0; r < M; ++r) gr += G[i][r] * sh.Rtinv[r][q];
-                    s += gr * G[j][q];
-                }
-                e.C[i][j] = s;
-            }
-    }
-};
+    __syncwarp();
+}
 
-// Riccati phase, kernel 1 of 3: every thread folds its chunk of elements into
-// one aggregate (suffix order), then the CTA runs an inclusive Hillis-Steele
-// suffix scan over its threads' aggregates.  Threads past the last element
-// hold the identity.
+// Base element e_k = (F, G Rt^-1 G', 2 Qb) from the slice's F, G; zero for
+// the terminal element.
+template <int N, int M>
+__device__ __forceinline__ void warp_base(bool terminal, const LqrShared<N, M>& sh, double* e,
+                                          RwWarp<N, M>& w, int lane) {
+    constexpr int NN = N * N;
+    for (int idx = lane; idx < NN; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        if (terminal) {
+            e[idx] = e[NN + idx] = e[2 * NN + idx] = 0.0;
+            continue;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+            double gr = 0.0;
+#pragma unroll
+            for (int r = 0; r < M; ++r) gr += w.G[i * M + r] * sh.Rtinv[r][q];
+            s += gr * w.G[j * M + q];
+        }
+        e[idx] = w.F[idx];
+        e[NN + idx] = s;
+        e[2 * NN + idx] = 2.0 * sh.Qb[i][j];
+    }
+    __syncwarp();
+}
+
+template <int N>
+__device__ __forceinline__ void warp_identity(double* e, int lane) {
+    constexpr int NN = N * N;
+    for (int idx = lane; idx < NN; idx += 32) {
+        e[idx] = (idx / N == idx % N) ? 1.0 : 0.0;
+        e[NN + idx] = 0.0;
+        e[2 * NN + idx] = 0.0;
+    }
+    __syncwarp();
+}
+
+template <int N>
+__device__ __forceinline__ void warp_copy(const double* src, double* dst, int lane) {
+    for (int idx = lane; idx < 3 * N * N; idx += 32) dst[idx] = __ldcg(src + idx);
+    __syncwarp();
+}
+
+template <int N>
+__device__ __forceinline__ void warp_store(const double* src, double* dst, int lane) {
+    for (int idx = lane; idx < 3 * N * N; idx += 32) dst[idx] = src[idx];
+    __syncwarp();
+}
+
+// K1: chunk aggregates + in-CTA suffix scan over warps.
 template <int N, int M, class Jac>
 __device__ void riccati_k1(const Jac& jac, const RicArgs& p) {
     constexpr int ESZ = elemr_doubles<N>();
-    __shared__ LqrShared<N, M> sh;
+    extern __shared__ __align__(16) unsigned char rw_smem[];
+    LqrShared<N, M>& sh = *reinterpret_cast<LqrShared<N, M>*>(rw_smem);
+    RwWarp<N, M>* slices = reinterpret_cast<RwWarp<N, M>*>(rw_smem + sizeof(LqrShared<N, M>));
     lqr_shared_init<N, M>(sh, p.Q, p.R, p.dt);
-    const RicSteps<N, M, Jac> st{jac, sh, p.T, p.dt};
-    const int t = blockIdx.x * RIC_BLOCK + threadIdx.x;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    RwWarp<N, M>& w = slices[wl];
+    const int gw = blockIdx.x * RW_WARPS + wl;
     const int total = p.T + 1;
-    const int lo = t * p.L, hi = min(lo + p.L, total);
-    if (t == 0) *p.fail = -1;
-    ElemR<N> acc;
+    const int lo = gw * p.L, hi = min(lo + p.L, total);
+    if (gw == 0 && lane == 0) *p.fail = -1;
+    double* acc = w.E[0];
+    double* e = w.E[1];
+    double* out = w.E[2];
     if (lo < total) {
-        ElemR<N> e, tmp;
-        st.base(hi - 1, acc);
+        const int k0 = hi - 1;
+        if (k0 < p.T) warp_fg<N, M>(jac, k0, p.dt, w, lane);
+        warp_base<N, M>(k0 >= p.T, sh, acc, w, lane);
         for (int k = hi - 2; k >= lo; --k) {
-            st.base(k, e);
-            elemr_combine<N>(e, acc, tmp);
-            acc = tmp;
+            warp_fg<N, M>(jac, k, p.dt, w, lane);  // k < T here
+            warp_base<N, M>(false, sh, e, w, lane);
+            warp_combine<N, M>(e, acc, out, w, lane);
+            double* t = acc;
+            acc = out;
+            out = t;
         }
     } else {
-        elemr_identity<N>(acc);
+        warp_identity<N>(acc, lane);
     }
     double* src = p.agg;
-    double* dst = p.agg + (size_t)p.nthr * ESZ;
-    elemr_store<N>(src + (size_t)t * ESZ, acc);
+    double* dst = p.agg + (size_t)p.nwarp * ESZ;
+    warp_store<N>(acc, src + (size_t)gw * ESZ, lane);
     __syncthreads();
-    for (int s = 1; s < RIC_BLOCK; s <<= 1) {
-        if (threadIdx.x + s < RIC_BLOCK) {
-            ElemR<N> b, o;
-            elemr_load<N>(src + (size_t)(t + s) * ESZ, b);
-            elemr_combine<N>(acc, b, o);
-            acc = o;
+    for (int s = 1; s < RW_WARPS; s <<= 1) {
+        if (wl + s < RW_WARPS) {
+            warp_copy<N>(src + (size_t)(gw + s) * ESZ, e, lane);
+            warp_combine<N, M>(acc, e, out, w, lane);
+            double* t = acc;
+            acc = out;
+            out = t;
         }
-        elemr_store<N>(dst + (size_t)t * ESZ, acc);
+        warp_store<N>(acc, dst + (size_t)gw * ESZ, lane);
         __syncthreads();
-        double* tt = src;
+        double* t = src;
         src = dst;
-        dst = tt;
+        dst = t;
     }
-    // the CTA aggregate (suffix of its first thread) feeds kernel 2
-    if (threadIdx.x == 0) elemr_store<N>(p.bagg + (size_t)blockIdx.x * ESZ, acc);
+    if (wl == 0) warp_store<N>(acc, p.bagg + (size_t)blockIdx.x * ESZ, lane);
 }
 
-// Kernel 2 of 3 (one CTA): inclusive suffix scan over the CTA aggregates.
-template <int N>
+// K2 (one CTA of RW_K2_WARPS warps): inclusive suffix scan over the CTA
+// aggregates, Hillis-Steele with each warp handling several items per round.
+template <int N, int M>
 __device__ void riccati_k2(const RicArgs& p) {
     constexpr int ESZ = elemr_doubles<N>();
+    extern __shared__ __align__(16) unsigned char rw_smem[];
+    RwWarp<N, M>* slices = reinterpret_cast<RwWarp<N, M>*>(rw_smem + sizeof(LqrShared<N, M>));
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    RwWarp<N, M>& w = slices[wl];
     double* src = p.bagg;
     double* dst = p.bagg + (size_t)p.nblk * ESZ;
-    const int b = threadIdx.x;
     for (int s = 1; s < p.nblk; s <<= 1) {
-        if (b < p.nblk) {
-            ElemR<N> a;
-            elemr_load<N>(src + (size_t)b * ESZ, a);
+        for (int b = wl; b < p.nblk; b += RW_K2_WARPS) {
             if (b + s < p.nblk) {
-                ElemR<N> c, o;
-                elemr_load<N>(src + (size_t)(b + s) * ESZ, c);
-                elemr_combine<N>(a, c, o);
-                elemr_store<N>(dst + (size_t)b * ESZ, o);
+                warp_copy<N>(src + (size_t)b * ESZ, w.E[0], lane);
+                warp_copy<N>(src + (size_t)(b + s) * ESZ, w.E[1], lane);
+                warp_combine<N, M>(w.E[0], w.E[1], w.E[2], w, lane);
+                warp_store<N>(w.E[2], dst + (size_t)b * ESZ, lane);
             } else {
-                elemr_store<N>(dst + (size_t)b * ESZ, a);
+                for (int idx = lane; idx < ESZ; idx += 32)
+                    dst[(size_t)b * ESZ + idx] = __ldcg(src + (size_t)b * ESZ + idx);
             }
         }
         __syncthreads();
-        double* tt = src;
+        double* t = src;
         src = dst;
-        dst = tt;
+        dst = t;
     }
 }
 
-// Kernel 3 of 3: each thread forms J_{hi} (the value matrix after its chunk)
-// from the in-CTA suffix of the next thread and the suffix of the next CTAs,
-// then re-walks its chunk in information form emitting the gains.
+// K3: J after the chunk, then the information-form re-walk emitting the gains.
 template <int N, int M, class Jac>
 __device__ void riccati_k3(const Jac& jac, const RicArgs& p) {
     constexpr int ESZ = elemr_doubles<N>();
-    __shared__ LqrShared<N, M> sh;
+    constexpr int NN = N * N;
+    extern __shared__ __align__(16) unsigned char rw_smem[];
+    LqrShared<N, M>& sh = *reinterpret_cast<LqrShared<N, M>*>(rw_smem);
+    RwWarp<N, M>* slices = reinterpret_cast<RwWarp<N, M>*>(rw_smem + sizeof(LqrShared<N, M>));
     lqr_shared_init<N, M>(sh, p.Q, p.R, p.dt);
-    const RicSteps<N, M, Jac> st{jac, sh, p.T, p.dt};
-    const int t = blockIdx.x * RIC_BLOCK + threadIdx.x;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    RwWarp<N, M>& w = slices[wl];
+    const int gw = blockIdx.x * RW_WARPS + wl;
     const int total = p.T + 1;
-    const int lo = t * p.L, hi = min(lo + p.L, total);
+    const int lo = gw * p.L, hi = min(lo + p.L, total);
     if (lo >= total) return;
-    const double* tsuf = p.agg + (size_t)(hs_rounds(RIC_BLOCK) & 1) * p.nthr * ESZ;
+    const double* wsuf = p.agg + (size_t)(hs_rounds(RW_WARPS) & 1) * p.nwarp * ESZ;
     const double* bsuf = p.bagg + (size_t)(hs_rounds(p.nblk) & 1) * p.nblk * ESZ;
-    const bool next_thread = threadIdx.x + 1 < RIC_BLOCK;
+    const bool next_warp = wl + 1 < RW_WARPS;
     const bool next_block = blockIdx.x + 1 < p.nblk;
-    double J2[N][N];
-    if (next_thread && next_block) {
-        ElemR<N> a, b, o;
-        elemr_load<N>(tsuf + (size_t)(t + 1) * ESZ, a);
-        elemr_load<N>(bsuf + (size_t)(blockIdx.x + 1) * ESZ, b);
-        elemr_combine<N>(a, b, o);
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int j = 0; j < N; ++j) J2[i][j] = o.J[i][j];
-    } else if (next_thread || next_block) {
-        const double* sp = next_thread ? tsuf + (size_t)(t + 1) * ESZ
-                                       : bsuf + (size_t)(blockIdx.x + 1) * ESZ;
-#pragma unroll
-        for (int i = 0; i < N * N; ++i) (&J2[0][0])[i] = __ldcg(sp + 2 * N * N + i);
+    if (next_warp && next_block) {
+        warp_copy<N>(wsuf + (size_t)(gw + 1) * ESZ, w.E[0], lane);
+        warp_copy<N>(bsuf + (size_t)(blockIdx.x + 1) * ESZ, w.E[1], lane);
+        warp_combine<N, M>(w.E[0], w.E[1], w.E[2], w, lane);
+        for (int idx = lane; idx < NN; idx += 32) w.J2[idx] = w.E[2][2 * NN + idx];
+    } else if (next_warp || next_block) {
+        const double* sp = next_warp ? wsuf + (size_t)(gw + 1) * ESZ
+                                     : bsuf + (size_t)(blockIdx.x + 1) * ESZ;
+        for (int idx = lane; idx < NN; idx += 32) w.J2[idx] = __ldcg(sp + 2 * NN + idx);
     } else {
-#pragma unroll
-        for (int i = 0; i < N * N; ++i) (&J2[0][0])[i] = 0.0;
+        for (int idx = lane; idx < NN; idx += 32) w.J2[idx] = 0.0;
     }
+    __syncwarp();
     int local_fail = -1;
-    for (int k = hi - 1; k >= lo; --k) {
-        if (k >= p.T) continue;
-        double F[N][N], G[N][M];
-        st.fg(k, F, G);
-        // H = Rb + G' P' G, [K | Lg] = H^-1 [G' P' F | G'],  P' = J2 / 2
-        double PG[N][M], PF[N][N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-#pragma unroll
-            for (int j = 0; j < M; ++j) {
+    const size_t TT = (size_t)p.T;
+    for (int k = min(hi, p.T) - 1; k >= lo; --k) {
+        warp_fg<N, M>(jac, k, p.dt, w, lane);
+        // PG = P' G, PF = P' F with P' = J2 / 2 (PF kept in W's left half)
+        for (int idx = lane; idx < N * M + NN; idx += 32) {
+            if (idx < N * M) {
+                const int i = idx / M, j = idx % M;
                 double s = 0.0;
 #pragma unroll
-                for (int q = 0; q < N; ++q) s += J2[i][q] * G[q][j];
-                PG[i][j] = 0.5 * s;
-            }
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
+                for (int q = 0; q < N; ++q) s += w.J2[i * N + q] * w.G[q * M + j];
+                w.PG[idx] = 0.5 * s;
+            } else {
+                const int e2 = idx - N * M, i = e2 / N, j = e2 % N;
                 double s = 0.0;
 #pragma unroll
-                for (int q = 0; q < N; ++q) s += J2[i][q] * F[q][j];
-                PF[i][j] = 0.5 * s;
+                for (int q = 0; q < N; ++q) s += w.J2[i * N + q] * w.F[q * N + j];
+                w.Tm[e2] = 0.5 * s;
             }
         }
-        double H[M][M], rhs[M][2 * N];
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-#pragma unroll
-            for (int j = 0; j < M; ++j) {
+        __syncwarp();
+        // H = Rb + G' PG,  rhs = [G' PF | G']
+        for (int idx = lane; idx < M * M + M * 2 * N; idx += 32) {
+            if (idx < M * M) {
+                const int i = idx / M, j = idx % M;
                 double s = 0.0;
 #pragma unroll
-                for (int q = 0; q < N; ++q) s += G[q][i] * PG[q][j];
-                H[i][j] = sh.Rb[i][j] + s;
-            }
+                for (int q = 0; q < N; ++q) s += w.G[q * M + i] * w.PG[q * M + j];
+                w.H[idx] = sh.Rb[i][j] + s;
+            } else {
+                const int e2 = idx - M * M, i = e2 / (2 * N), j = e2 % (2 * N);
+                double s;
+                if (j < N) {
+                    s = 0.0;
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < N; ++q) s += G[q][i] * PF[q][j];
-                rhs[i][j] = s;
-                rhs[i][N + j] = G[j][i];
-            }
-        }
-#pragma unroll
-        for (int col = 0; col < M; ++col) {  // Gaussian elimination, partial pivoting
-            int pv = col;
-#pragma unroll
-            for (int r = col + 1; r < M; ++r)
-                if (fabs(H[r][col]) > fabs(H[pv][col])) pv = r;
-            if (pv != col) {
-#pragma unroll
-                for (int q = 0; q < M; ++q) {
-                    const double tq = H[col][q];
-                    H[col][q] = H[pv][q];
-                    H[pv][q] = tq;
+                    for (int q = 0; q < N; ++q) s += w.G[q * M + i] * w.Tm[q * N + j];
+                } else {
+                    s = w.G[(j - N) * M + i];
                 }
+                w.rhs[e2] = s;
+            }
+        }
+        __syncwarp();
+        warp_gauss_jordan<M, 2 * N>(w.H, w.rhs, lane);  // rhs <- [K | H^-1 G']
+        // outputs; Mt = I + C_k J2 with C_k = G Rt^-1 G'; W = F (Phi solve)
+        for (int idx = lane; idx < M * N; idx += 32) {
+            const int i = idx / N, j = idx % N;
+            p.K[(size_t)idx * TT + k] = w.rhs[i * 2 * N + j];
+            p.Lg[(size_t)idx * TT + k] = w.rhs[i * 2 * N + N + j];
+        }
+        for (int idx = lane; idx < NN; idx += 32) {
+            const int i = idx / N, j = idx % N;
+            double s = 0.0;
 #pragma unroll
-                for (int q = 0; q < 2 * N; ++q) {
-                    const double tq = rhs[col][q];
-                    rhs[col][q] = rhs[pv][q];
-                    rhs[pv][q] = tq;
+            for (int q = 0; q < M; ++q) s += w.G[i * M + q] * w.rhs[q * 2 * N + j];
+            p.Acl[(size_t)idx * TT + k] = w.F[idx] - s;
+            // C_k J2: C_k = G Rt^-1 G'
+            double cj = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+                double c = 0.0;
+#pragma unroll
+                for (int a = 0; a < M; ++a) {
+                    double gr = 0.0;
+#pragma unroll
+                    for (int r = 0; r < M; ++r) gr += w.G[i * M + r] * sh.Rtinv[r][a];
+                    c += gr * w.G[q * M + a];
                 }
+                cj += c * w.J2[q * N + j];
             }
-#pragma unroll
-            for (int r = col + 1; r < M; ++r) {
-                const double l = H[r][col] / H[col][col];
-#pragma unroll
-                for (int q = col; q < M; ++q) H[r][q] -= l * H[col][q];
-#pragma unroll
-                for (int q = 0; q < 2 * N; ++q) rhs[r][q] -= l * rhs[col][q];
-            }
+            w.Mt[idx] = cj;
+            w.W[i * N + j] = w.F[idx];  // N x N right-hand side
         }
+        for (int idx = lane; idx < N * M; idx += 32) p.Gm[(size_t)idx * TT + k] = w.G[idx];
+        __syncwarp();
+        warp_gauss_jordan<N, N>(w.Mt, w.W, lane);  // W <- Phi = (I + C J2)^-1 F
+        // JF = J2 F (into JA), then J_k = Phi' JF + 2 Qb, symmetrised
+        for (int idx = lane; idx < NN; idx += 32) {
+            const int i = idx / N, j = idx % N;
+            double s = 0.0;
 #pragma unroll
-        for (int r = M - 1; r >= 0; --r)
-#pragma unroll
-            for (int q = 0; q < 2 * N; ++q) {
-                double v = rhs[r][q];
-#pragma unroll
-                for (int c2 = r + 1; c2 < M; ++c2) v -= H[r][c2] * rhs[c2][q];
-                rhs[r][q] = v / H[r][r];
-            }
-        // per-step outputs, element-major ([element][T]): the affine scans
-        // read one element of consecutive steps per warp load
-        const size_t TT = (size_t)p.T;
-#pragma unroll
-        for (int i = 0; i < M; ++i)
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                p.K[(i * N + j) * TT + k] = rhs[i][j];
-                p.Lg[(i * N + j) * TT + k] = rhs[i][N + j];
-            }
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < M; ++q) s += G[i][q] * rhs[q][j];
-                p.Acl[(i * N + j) * TT + k] = F[i][j] - s;
-            }
-#pragma unroll
-            for (int j = 0; j < M; ++j) p.Gm[(i * M + j) * TT + k] = G[i][j];
+            for (int q = 0; q < N; ++q) s += w.J2[i * N + q] * w.F[q * N + j];
+            w.JA[idx] = s;
         }
-        // Phi = (I + C_k J2)^-1 F ; J_k = Phi' J2 F + 2 Qb
-        ElemR<N> e;
-        st.base_fg(F, G, e);
-        double X[N][N];
+        __syncwarp();
+        for (int idx = lane; idx < NN; idx += 32) {
+            const int i = idx / N, j = idx % N;
+            double s = 0.0;
 #pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int j = 0; j < N; ++j) X[i][j] = F[i][j];
-        solve_ipcj<N, N>(e.C, J2, X);
-        double JF[N][N], Jn[N][N];
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < N; ++q) s += J2[i][q] * F[q][j];
-                JF[i][j] = s;
-            }
+            for (int q = 0; q < N; ++q) s += w.W[q * N + i] * w.JA[q * N + j];
+            w.Tm[idx] = s + 2.0 * sh.Qb[i][j];
+        }
+        __syncwarp();
         bool finite = true;
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < N; ++q) s += X[q][i] * JF[q][j];
-                Jn[i][j] = s + 2.0 * sh.Qb[i][j];
-            }
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                J2[i][j] = 0.5 * (Jn[i][j] + Jn[j][i]);
-                finite = finite && isfinite(J2[i][j]);
-            }
+        for (int idx = lane; idx < NN; idx += 32) {
+            const int i = idx / N, j = idx % N;
+            const double v = 0.5 * (w.Tm[i * N + j] + w.Tm[j * N + i]);
+            w.J2[idx] = v;
+            finite = finite && isfinite(v);
+        }
+        finite = __all_sync(0xffffffffu, finite);
+        __syncwarp();
         if (!finite && local_fail < 0) local_fail = k;
     }
-    if (local_fail >= 0) atomicMax(p.fail, local_fail);
+    if (lane == 0 && local_fail >= 0) atomicMax(p.fail, local_fail);
 }
 
 // After kernel 3: publish a Riccati blow-up to the planner status word.
@@ -533,17 +660,17 @@ __device__ __forceinline__ void riccati_finish(const RicArgs& p) {
 }
 
 // Host: chunk length and grid of the Riccati phase for horizon T over
-// `max_blocks` CTAs.
+// `max_blocks` CTAs of RW_WARPS warps.
 struct RicGeom {
-    int L, nthr, nblk;
+    int L, nwarp, nblk;
 };
 inline RicGeom ric_geom(int T, int max_blocks) {
     const int total = T + 1;
-    const long cap = (long)max_blocks * RIC_BLOCK;
-    int L = (int)std::max<long>(RIC_MIN_CHUNK, (total + cap - 1) / cap);
+    const long cap = (long)max_blocks * RW_WARPS;
+    int L = (int)std::max<long>(RW_MIN_CHUNK, (total + cap - 1) / cap);
     const int used = (total + L - 1) / L;
-    const int nblk = (used + RIC_BLOCK - 1) / RIC_BLOCK;
-    return RicGeom{L, nblk * RIC_BLOCK, nblk};
+    const int nblk = (used + RW_WARPS - 1) / RW_WARPS;
+    return RicGeom{L, nblk * RW_WARPS, nblk};
 }
 
 }  // namespace fcb

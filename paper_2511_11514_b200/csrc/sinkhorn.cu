@@ -57,9 +57,6 @@ constexpr double EXP_CLIP = 500.0;       // sinkhorn.py:67
 constexpr double OMEGA_FLOOR = 1e-12;    // sinkhorn.py:66
 constexpr double AUTO_OMEGA_FACTOR = 0.05;  // sinkhorn.py:65
 
-// scal[] layout (device double[16])
-enum { SC_OMEGA = 0, SC_S = 1, SC_C = 2 /*2..4*/, SC_MX2 = 5, SC_MX = 6 /*6..8*/, SC_MY2 = 9,
-       SC_MY = 10 /*10..12*/ };
 
 struct Sweep {
     int rows, cols, cols8;   // cols8: columns rounded up to OT_SUB
@@ -98,6 +95,10 @@ struct OtArgs {
     double* stat;
     double* bary;
     const int* gate;
+    // SWEEP-mode epilogue (fcb_lse_sweep): out = epi_scale omega (epi_shift - L)
+    // when epi_scale != 0, else L; bary_L stores L (not 1) in bary[i][0]
+    double epi_scale, epi_shift;
+    int bary_L;
 };
 
 // ---------------------------------------------------------------------------
@@ -615,10 +616,10 @@ __device__ __forceinline__ void sweep_only_pass(const OtArgs<Real>& p, const OtS
     double* out = p.f_out;
     double* bo = p.bary;
     merge_phase<Real, D, BARY>(p.B, p.pm, p.ps, p.pa, [&](int i, double L, const double* bar) {
-        out[i] = L;
+        if (out) out[i] = (p.epi_scale != 0.0) ? p.epi_scale * sc.w * (p.epi_shift - L) : L;
         if (BARY && bo) {  // weighted mean of the columns (M-shard combine)
             double* o = bo + (size_t)i * (D + 1);
-            o[0] = 1.0;
+            o[0] = p.bary_L ? L : 1.0;
             for (int q = 0; q < D; ++q) o[1 + q] = bar[q] / csc + c[q];
         }
     });
@@ -1040,11 +1041,16 @@ static void ot_layout(OtLayout<Real>& L, int mode, int n, int m, int d, int rpt,
     L.bytes = ar.off + 256;
 }
 
+struct OtEpi {
+    double scale = 0.0, shift = 0.0;
+    int bary_L = 0;
+};
+
 template <typename Real, int D, int RPT, bool BARY>
 static int ot_launch(int mode, const double* X, int n, const double* Y, int m, const double* scal,
                      int max_iters, double tol, const double* f0, double* f, double* g,
                      double* rs, double* stat, double* bary, const int* gate, void* ws,
-                     size_t ws_bytes, cudaStream_t st) {
+                     size_t ws_bytes, cudaStream_t st, OtEpi epi = OtEpi{}) {
     int grid = 0;
     int rc = ot_grid_size<Real, D, RPT, BARY>(&grid);
     if (rc) return rc;
@@ -1066,6 +1072,9 @@ static int ot_launch(int mode, const double* X, int n, const double* Y, int m, c
     a.stat = stat;
     a.bary = bary;
     a.gate = gate;
+    a.epi_scale = epi.scale;
+    a.epi_shift = epi.shift;
+    a.bary_L = epi.bary_L;
     FCB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(GridBarrier), st));
     void* args[] = {&a};
     FCB_CUDA(cudaLaunchCooperativeKernel((const void*)ot_solve_kernel<Real, D, RPT, BARY>,
@@ -1136,6 +1145,48 @@ int ot_solve(int mode, int precision, const double* X, int n, const double* Y, i
                                             stat, bary, gate, ws, ws_bytes, st);
     return ot_dispatch<float, RPT_F32>(mode, d, X, n, Y, m, scal, max_iters, tol, f0, f, g, rs,
                                        stat, bary, gate, ws, ws_bytes, st);
+}
+
+// One LSE sweep with an epilogue (M-sharded solves, distributed.py):
+//   L_i = LSE_j((pot_j - |r_i - s_j|^2) / omega)            (sinkhorn.py:151-167)
+//   out_i = scale omega (shift - L_i)  (scale != 0)   or   L_i
+//   bary (nullable, nr x (d+1)): {L_i, softmax-weighted mean of the columns}
+template <typename Real, int RPT>
+static int lse_sweep_t(int d, const double* R, int nr, const double* S, int ns, const double* scal,
+                       const double* pot, double* out, double* bary, const int* gate, void* ws,
+                       size_t ws_bytes, cudaStream_t st, OtEpi epi) {
+#define FCB_LS_CASE(DD)                                                                           \
+    if (d == DD) {                                                                                \
+        if (bary)                                                                                 \
+            return ot_launch<Real, DD, RPT, true>(FCB_OT_SWEEP, R, nr, S, ns, scal, 1, 0.0, pot,   \
+                                                  out, nullptr, nullptr, nullptr, bary, gate, ws, \
+                                                  ws_bytes, st, epi);                             \
+        return ot_launch<Real, DD, RPT, false>(FCB_OT_SWEEP, R, nr, S, ns, scal, 1, 0.0, pot, out, \
+                                               nullptr, nullptr, nullptr, nullptr, gate, ws,      \
+                                               ws_bytes, st, epi);                                \
+    }
+    FCB_LS_CASE(1)
+    FCB_LS_CASE(2)
+    FCB_LS_CASE(3)
+#undef FCB_LS_CASE
+    return fail(FCB_ENOTSUP, "point dimension must be 1, 2 or 3");
+}
+
+int lse_sweep(int precision, const double* R, int nr, const double* S, int ns, int d,
+              const double* scal, const double* pot, double out_scale, double out_shift,
+              double* out, double* bary, const int* gate, void* ws, size_t ws_bytes,
+              cudaStream_t st) {
+    if (nr < 1 || ns < 1) return fail(FCB_EINPUT, "empty point set");
+    if (!pot) return fail(FCB_EINPUT, "sweep needs a potential");
+    OtEpi epi;
+    epi.scale = out_scale;
+    epi.shift = out_shift;
+    epi.bary_L = 1;
+    if (precision == FCB_FP64)
+        return lse_sweep_t<double, RPT_F64>(d, R, nr, S, ns, scal, pot, out, bary, gate, ws,
+                                            ws_bytes, st, epi);
+    return lse_sweep_t<float, RPT_F32>(d, R, nr, S, ns, scal, pot, out, bary, gate, ws, ws_bytes,
+                                       st, epi);
 }
 
 size_t omega_ws_bytes(int n, int m) {

@@ -118,7 +118,71 @@ struct MedState {
     unsigned long long prefix[2];  // selected high bits so far (lo, hi target)
     unsigned long long rank[2];    // remaining rank inside the prefix bucket
     unsigned long long hist[2][MED_BINS];
+    unsigned done;                 // CTAs finished with the current pass
 };
+
+// The digit selection of one radix pass, by one CTA of MED_BLOCK threads:
+// each thread owns MED_BINS / MED_BLOCK consecutive bins, a block-wide
+// exclusive scan of the per-thread counts locates the bin holding each target
+// rank.  Then the histograms are cleared for the next pass.
+__device__ void median_select_block(MedState* st, int n, int pass) {
+    constexpr int PER = MED_BINS / MED_BLOCK;
+    __shared__ unsigned long long s_warp[MED_BLOCK / 32];
+    __shared__ unsigned long long s_new[2][2];  // {prefix, rank} per target
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int bits = c_med_bits[pass];
+    const int nbins = 1 << bits;
+    const unsigned long long p0 = st->prefix[0], p1 = st->prefix[1];
+    const bool same = p0 == p1;
+    for (int t = 0; t < 2; ++t) {
+        const unsigned long long* h = st->hist[same ? 0 : t];
+        const unsigned long long pre = t ? p1 : p0;
+        // the n diagonal zeros live in bucket 0 while the prefix is 0
+        const unsigned long long zeros = (pre == 0ull) ? (unsigned long long)n : 0ull;
+        unsigned long long c[PER], sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int b = tid * PER + k;
+            c[k] = (b < nbins) ? __ldcg(h + b) + (b == 0 ? zeros : 0ull) : 0ull;
+            sum += c[k];
+        }
+        unsigned long long incl = sum;  // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) s_warp[wid] = incl;
+        __syncthreads();
+        unsigned long long base = 0;
+        for (int w = 0; w < wid; ++w) base += s_warp[w];
+        const unsigned long long excl = base + incl - sum;
+        const unsigned long long r = st->rank[t];
+        const bool last = tid == MED_BLOCK - 1;
+        if ((r >= excl && r < excl + sum) || (last && r >= excl + sum)) {
+            unsigned long long rr = r - excl;
+            int b = tid * PER;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                if (rr < c[k] || k == PER - 1) break;
+                rr -= c[k];
+                ++b;
+            }
+            b = min(b, nbins - 1);  // past the end only for inconsistent counts
+            s_new[t][0] = (pre << bits) | (unsigned long long)b;
+            s_new[t][1] = rr;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        st->prefix[0] = s_new[0][0];
+        st->rank[0] = s_new[0][1];
+        st->prefix[1] = s_new[1][0];
+        st->rank[1] = s_new[1][1];
+        st->done = 0u;
+    }
+    for (int b = tid; b < 2 * MED_BINS; b += MED_BLOCK) (&st->hist[0][0])[b] = 0ull;
+}
 
 template <int D>
 __device__ __forceinline__ unsigned long long sqdist_key(const double* a, const double* b) {
@@ -187,6 +251,15 @@ __global__ void __launch_bounds__(MED_BLOCK) median_hist_kernel(const double* __
         if (hist[0][b]) atomicAdd(&st->hist[0][b], (unsigned long long)hist[0][b]);
         if (!same && hist[1][b]) atomicAdd(&st->hist[1][b], (unsigned long long)hist[1][b]);
     }
+    // the last CTA of the pass selects the digit (no separate launch)
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(&st->done, 1u) == gridDim.x - 1) ? 1 : 0;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    median_select_block(st, n, pass);
 }
 
 __global__ void median_init_kernel(MedState* st, unsigned long long klo, unsigned long long khi,
@@ -197,33 +270,8 @@ __global__ void median_init_kernel(MedState* st, unsigned long long klo, unsigne
         st->prefix[0] = st->prefix[1] = 0ull;
         st->rank[0] = klo;
         st->rank[1] = khi;
+        st->done = 0u;
     }
-}
-
-__global__ void median_select_kernel(MedState* st, int n, int pass, const int* gate) {
-    if (gate && *((volatile const int*)gate) != 0) return;
-    if (threadIdx.x == 0) {
-        const int bits = c_med_bits[pass];
-        const int nbins = 1 << bits;
-        const bool same = st->prefix[0] == st->prefix[1];
-        for (int t = 0; t < 2; ++t) {
-            unsigned long long* h = st->hist[same ? 0 : t];
-            // the n diagonal zeros live in bucket 0 while the prefix is 0
-            const unsigned long long zeros = (st->prefix[t] == 0ull) ? (unsigned long long)n : 0ull;
-            unsigned long long r = st->rank[t];
-            int b = 0;
-            for (; b < nbins; ++b) {
-                const unsigned long long c = h[b] + (b == 0 ? zeros : 0ull);
-                if (r < c) break;
-                r -= c;
-            }
-            if (b >= nbins) b = nbins - 1;  // unreachable for consistent counts
-            st->rank[t] = r;
-            st->prefix[t] = (st->prefix[t] << bits) | (unsigned long long)b;
-        }
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < 2 * MED_BINS; b += blockDim.x) (&st->hist[0][0])[b] = 0ull;
 }
 
 __global__ void median_finish_kernel(const MedState* st, int n, double log_np1, double* hstat,
@@ -285,8 +333,6 @@ int median_bandwidth(const double* X, int n, int d, double log_np1, double* hsta
             default: return fail(FCB_ENOTSUP, "dimension must be 1, 2 or 3");
         }
         FCB_LAUNCHED("median_hist_kernel");
-        median_select_kernel<<<1, 256, 0, st>>>(ms, n, pass, gate);
-        FCB_LAUNCHED("median_select_kernel");
     }
     median_finish_kernel<<<1, 32, 0, st>>>(ms, n, log_np1, hstat, gate);
     FCB_LAUNCHED("median_finish_kernel");
@@ -311,10 +357,12 @@ struct SvPlan {
     int n, nrb, nchunks, chunk_len, items, n8;
 };
 
-static SvPlan sv_plan(int n, int rpt, int grid) {
+// rows n (queries), columns nc (sources; default: the same n points)
+static SvPlan sv_plan(int n, int rpt, int grid, int nc = -1) {
     SvPlan p{};
     p.n = n;
-    p.n8 = (n + SV_SUB - 1) / SV_SUB * SV_SUB;
+    if (nc < 0) nc = n;
+    p.n8 = (nc + SV_SUB - 1) / SV_SUB * SV_SUB;
     const int br = SV_BLOCK * rpt;
     p.nrb = (n + br - 1) / br;
     const int maxch = std::max(1, std::min(SV_MAXCH, p.n8 / 64));
@@ -468,6 +516,66 @@ __global__ void sv_merge_kernel(SvPlan pl, const Real* __restrict__ part,
 constexpr int SV_RPT_F32 = 2;
 constexpr int SV_RPT_F64 = 1;
 
+// Sharded sources (fcb_stein_partial): query rows are all n points, source
+// columns the points [col0, col0 + nc); centred on X[0] like stein_run.
+template <typename Real, int D>
+__global__ void sv_pack_range_kernel(const double* __restrict__ X, int n, int col0, int nc,
+                                     int nc8, const double* __restrict__ score,
+                                     const double* __restrict__ hstat,
+                                     SvCol<Real>* __restrict__ cols, Vec4<Real>* __restrict__ rows,
+                                     const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    const double h = hstat[0];
+    const double unit = (sizeof(Real) == 4) ? kLog2e : 1.0;
+    const double sc = sqrt(unit / h);
+    const int tot = max(n, nc8);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < tot; j += gridDim.x * blockDim.x) {
+        if (j < n) {
+            Real xs[3] = {0, 0, 0};
+            for (int q = 0; q < D; ++q) xs[q] = (Real)((X[(size_t)j * D + q] - X[q]) * sc);
+            rows[j] = Vec4<Real>{xs[0], xs[1], xs[2], 0};
+        }
+        if (j < nc8) {
+            SvCol<Real> c{};
+            if (j < nc) {
+                const size_t g = (size_t)(col0 + j);
+                for (int q = 0; q < D; ++q) {
+                    const double xc = X[g * D + q] - X[q];
+                    c.x[q] = (Real)(xc * sc);
+                    c.w[q] = (Real)(score[g * D + q] - (2.0 / h) * xc);
+                }
+            } else {
+                for (int q = 0; q < 4; ++q) {
+                    c.x[q] = (Real)1e30;
+                    c.w[q] = 0;
+                }
+            }
+            cols[j] = c;
+        }
+    }
+}
+
+// Raw per-row sums over the source chunks: out[i] = {sum_j k_ij, sum_j k_ij w_j}.
+template <typename Real, int D>
+__global__ void sv_merge_raw_kernel(SvPlan pl, const Real* __restrict__ part,
+                                    double* __restrict__ out, const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    const int n = pl.n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double K = 0.0, A[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) A[q] = 0.0;
+        for (int ch = 0; ch < pl.nchunks; ++ch) {
+            K += (double)part[((size_t)ch * (D + 1)) * n + i];
+#pragma unroll
+            for (int q = 0; q < D; ++q) A[q] += (double)part[((size_t)ch * (D + 1) + 1 + q) * n + i];
+        }
+        out[(size_t)i * (D + 1)] = K;
+#pragma unroll
+        for (int q = 0; q < D; ++q) out[(size_t)i * (D + 1) + 1 + q] = A[q];
+    }
+}
+
 struct SvWs {
     double* centre;
     void* cols;
@@ -544,6 +652,57 @@ int stein_flow(int precision, const double* X, int n, int d, const double* score
     FCB_SV_CASE(2)
     FCB_SV_CASE(3)
 #undef FCB_SV_CASE
+    return fail(FCB_ENOTSUP, "dimension must be 1, 2 or 3");
+}
+
+size_t stein_partial_ws_bytes(int precision, int n, int nc, int d) {
+    const int rpt = precision == FCB_FP64 ? SV_RPT_F64 : SV_RPT_F32;
+    SvPlan pl = sv_plan(n, rpt, sv_grid(), nc);
+    return sv_layout(precision, std::max(n, pl.n8), d, pl, nullptr, 0).total;
+}
+
+template <typename Real, int D, int RPT>
+static int stein_partial_run(const double* X, int n, int col0, int nc, const double* scores,
+                             const double* hstat, double* out, const int* gate, void* ws,
+                             size_t ws_bytes, cudaStream_t st) {
+    const int precision = sizeof(Real) == 8 ? FCB_FP64 : FCB_FP32;
+    SvPlan pl = sv_plan(n, RPT, sv_grid(), nc);
+    SvWs L = sv_layout(precision, std::max(n, pl.n8), D, pl, ws, ws_bytes);
+    if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "stein_partial workspace too small");
+    const int pb = std::max(1, std::min(4 * sm_count(), (std::max(n, pl.n8) + 255) / 256));
+    sv_pack_range_kernel<Real, D><<<pb, 256, 0, st>>>(X, n, col0, nc, pl.n8, scores, hstat,
+                                                     static_cast<SvCol<Real>*>(L.cols),
+                                                     static_cast<Vec4<Real>*>(L.rows), gate);
+    FCB_LAUNCHED("sv_pack_range_kernel");
+    const int grid = std::min(pl.items, sv_grid());
+    sv_sweep_kernel<Real, D, RPT><<<grid, SV_BLOCK, 0, st>>>(
+        pl, static_cast<const Vec4<Real>*>(L.rows), static_cast<const SvCol<Real>*>(L.cols),
+        static_cast<Real*>(L.part), gate);
+    FCB_LAUNCHED("sv_sweep_kernel");
+    const int mb = std::max(1, std::min(4 * sm_count(), (n + 255) / 256));
+    sv_merge_raw_kernel<Real, D><<<mb, 256, 0, st>>>(pl, static_cast<const Real*>(L.part), out,
+                                                    gate);
+    FCB_LAUNCHED("sv_merge_raw_kernel");
+    return FCB_OK;
+}
+
+int stein_partial(int precision, const double* X, int n, int d, int col0, int nc,
+                  const double* scores, const double* hstat, double* out, const int* gate,
+                  void* ws, size_t ws_bytes, cudaStream_t st) {
+    if (n < 1 || nc < 1 || col0 < 0 || col0 + nc > n)
+        return fail(FCB_EINPUT, "stein_partial: bad source range");
+#define FCB_SP_CASE(DD)                                                                         \
+    if (d == DD) {                                                                              \
+        if (precision == FCB_FP64)                                                              \
+            return stein_partial_run<double, DD, SV_RPT_F64>(X, n, col0, nc, scores, hstat,     \
+                                                             out, gate, ws, ws_bytes, st);      \
+        return stein_partial_run<float, DD, SV_RPT_F32>(X, n, col0, nc, scores, hstat, out,     \
+                                                        gate, ws, ws_bytes, st);                \
+    }
+    FCB_SP_CASE(1)
+    FCB_SP_CASE(2)
+    FCB_SP_CASE(3)
+#undef FCB_SP_CASE
     return fail(FCB_ENOTSUP, "dimension must be 1, 2 or 3");
 }
 

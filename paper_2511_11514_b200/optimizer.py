@@ -192,9 +192,15 @@ def plan(
     q: ReferenceDistribution,
     disc: Discretization,
     cfg: PlanConfig = PlanConfig(),
+    *,
+    group=None,
 ) -> PlanResult:
-    """Synthesize a coverage trajectory for q (optimizer.py:171-304)."""
-    return plan_detailed(model, q, disc, cfg).result
+    """Synthesize a coverage trajectory for q (optimizer.py:171-304).
+
+    group (additive, keyword-only): shard the flow over the ranks of a
+    torch.distributed group (one GPU each); see plan_detailed.
+    """
+    return plan_detailed(model, q, disc, cfg, group=group).result
 
 
 def plan_detailed(
@@ -204,11 +210,17 @@ def plan_detailed(
     cfg: PlanConfig = PlanConfig(),
     poll_lag: int = 2,
     resident_targets: torch.Tensor | None = None,
+    group=None,
 ) -> PlanRun:
     """plan() plus the device-side record (inner iteration log, pair count).
 
     resident_targets: the transport targets already in device memory
     (float64, (M, d)); used by bench.py to time with inputs resident in HBM.
+    With `group`, this rank's shard of them.
+    group (additive, keyword): a torch.distributed process group, one rank per
+    GPU.  Every rank passes the same problem; the Sinkhorn reference samples
+    (or the SVGD sources) are sharded across the ranks (distributed.py) and
+    every rank returns the same PlanResult.  Rollout and LQR are replicated.
     """
     if cfg.method == "stein" and not isinstance(q, GaussianMixture):
         raise ValueError("the stein method needs a score-based (mixture) reference")
@@ -267,6 +279,11 @@ def plan_detailed(
     metric_vals = _dev.zeros((max(n_metric, 1), 4), device=dev)
     status_host = torch.zeros(8, dtype=torch.int32, pin_memory=True)
 
+    sharded = group is not None
+    if sharded:
+        from . import distributed as _dist
+
+        g_rank, g_world = _dist._world(group)
     if cfg.method == "sinkhorn":
         Y = targets.points
         if Y.shape[1] != d:
@@ -274,21 +291,31 @@ def plan_detailed(
 
             raise SinkhornInputError(f"point dims disagree: {d} vs {Y.shape[1]}")
         M = Y.shape[0]
-        Yd = resident_targets if resident_targets is not None else _dev.f64(Y, dev)
         scfg = cfg.sinkhorn
         prec = _precision.pick(scfg.precision, T * max(T, M), scfg.tol)
         warm_f, warm_p = _dev.zeros((T,), device=dev), _dev.zeros((T,), device=dev)
         warm_valid = torch.zeros(2, dtype=torch.int32, device=dev)
-        flow_ws = _dev.Workspace.get(lib.fcb_sinkhorn_flow_workspace_bytes(prec, T, M, d), "plan_flow")
         omega_fixed = _omega_arg(scfg.omega)
+        if sharded:
+            Yd = (resident_targets if resident_targets is not None
+                  else _dev.f64(_dist.shard_rows(Y, g_rank, g_world), dev))
+            shard_flow = _dist.ShardedSinkhorn(Yd, T, scfg, group, precision=prec)
+        else:
+            Yd = resident_targets if resident_targets is not None else _dev.f64(Y, dev)
+            flow_ws = _dev.Workspace.get(lib.fcb_sinkhorn_flow_workspace_bytes(prec, T, M, d),
+                                         "plan_flow")
     else:
         M = 0
         scfg_st = cfg.stein
         prec = _precision.pick(scfg_st.precision, T * T)
         gmm = q.device_params()
         bw_fixed = 0.0 if scfg_st.bandwidth == "median" else float(scfg_st.bandwidth)
-        flow_ws = _dev.Workspace.get(lib.fcb_stein_flow_full_workspace_bytes(prec, T, d), "plan_flow")
         log_np1 = math.log(T + 1.0)
+        if sharded:
+            shard_flow = _dist.ShardedStein(T, d, q, scfg_st.bandwidth, group, precision=prec)
+        else:
+            flow_ws = _dev.Workspace.get(lib.fcb_stein_flow_full_workspace_bytes(prec, T, d),
+                                         "plan_flow")
     upd_ws = _dev.Workspace.get(lib.fcb_plan_update_workspace_bytes(n_s, m_c, T), "plan_upd")
     roll_ws = _dev.Workspace.get(lib.fcb_rollout_workspace_bytes(n_s, T), "plan_roll")
     if want_metric:
@@ -318,7 +345,7 @@ def plan_detailed(
     # persistent launch (fcb_plan_fused) after iteration 0 has stored the
     # Riccati phase; anything it does not cover stays on the per-iteration path
     fused_ok = (os.environ.get("FCB_FUSED", "1") != "0" and cfg.method == "sinkhorn"
-                and not want_metric and prec == _lib.FCB_FP32
+                and not want_metric and prec == _lib.FCB_FP32 and not sharded
                 and d == 2 and maxit > 1 and spec.model_id in (
                     _lib.FCB_MODEL_SINGLE_INTEGRATOR_2D, _lib.FCB_MODEL_DOUBLE_INTEGRATOR_2D))
     fused_ran = False
@@ -359,7 +386,12 @@ def plan_detailed(
                  _dev.ptr(met_ws), met_ws.numel(), stream)
             e2 = torch.cuda.Event(enable_timing=True)
             e2.record()
-        if cfg.method == "sinkhorn":
+        if sharded and cfg.method == "sinkhorn":
+            shard_flow.flow_into(X, warm_f, warm_p, warm_valid, flow, fstat, state, it, flow_log,
+                                 float(cfg.convergence_tol))
+        elif sharded:
+            shard_flow.flow_into(X, flow, fstat, state, it, flow_log, float(cfg.convergence_tol))
+        elif cfg.method == "sinkhorn":
             call("fcb_sinkhorn_flow", prec, _dev.ptr(X), T, _dev.ptr(Yd), M, d, omega_fixed,
                  scfg.max_iters, scfg.tol, _dev.ptr(warm_f), _dev.ptr(warm_p),
                  _dev.ptr(warm_valid), _dev.ptr(flow), _dev.ptr(fstat), state_ptr, it,

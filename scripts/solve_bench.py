@@ -1,7 +1,7 @@
 """Per-iteration device time of the fp32 asymmetric / symmetric solve.
 
     python scripts/solve_bench.py            # config-sized shapes
-    FCB_OT_LEGACY=1 python scripts/solve_bench.py
+    FCB_OT_CTAS_PER_SM=1 python scripts/solve_bench.py
 """
 import os
 import sys
