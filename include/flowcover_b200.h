@@ -283,12 +283,16 @@ FCB_API int fcb_point_sums(const double* P, int n, int d, double* out, fcb_strea
  * (ns) with column potential pot: L_i = LSE_j((pot_j - |r_i - s_j|^2)/omega).
  * out (nullable) = out_scale omega (out_shift - L) when out_scale != 0, else
  * L (omega = scal[0]: the g-update w (log b - L) is out_scale 1, shift log b);
- * bary (nullable, nr*(d+1)) = {L_i, softmax-weighted mean of the columns}. */
+ * bary (nullable, nr*(d+1)) = {L_i, softmax-weighted mean of the columns}.
+ * row_est (nullable, nr): a potential of the rows whose fixed-point relation
+ * L_i = row_logw - row_est_i / omega shifts each row's terms near 1 (the fp32
+ * fast path needs it; without it the first pass runs the careful loop). */
 FCB_API size_t fcb_lse_sweep_workspace_bytes(int precision, int nr, int ns, int d);
 FCB_API int fcb_lse_sweep(int precision, const double* R, int nr, const double* S, int ns, int d,
-                          const double* scal, const double* pot, double out_scale,
-                          double out_shift, double* out, double* bary, const int* gate, void* ws,
-                          size_t ws_bytes, fcb_stream_t stream);
+                          const double* scal, const double* pot, const double* row_est,
+                          double row_logw, double out_scale, double out_shift, double* out,
+                          double* bary, const int* gate, void* ws, size_t ws_bytes,
+                          fcb_stream_t stream);
 
 /* Flow start: omega from X and the global Y sums ysum (d+2), both centrings
  * (scal_x: cross solve, scal_s: self solve; resolve_omega layout), f/p from

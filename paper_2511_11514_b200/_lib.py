@@ -105,7 +105,8 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "fcb_point_sums": (_I, [_P, _I, _I, _P, _P]),
     "fcb_lse_sweep_workspace_bytes": (_Z, [_I, _I, _I, _I]),
-    "fcb_lse_sweep": (_I, [_I, _P, _I, _P, _I, _I, _P, _P, _D, _D, _P, _P, _P, _P, _Z, _P]),
+    "fcb_lse_sweep": (_I, [_I, _P, _I, _P, _I, _I, _P, _P, _P, _D, _D, _D, _P, _P, _P, _P, _Z,
+                           _P]),
     "fcb_shard_init": (_I, [_I, _P, _I, _I, _P, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "fcb_shard_cross_merge": (
         _I, [_I, _I, _I, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -34,9 +34,9 @@
 namespace fcb {
 
 int lse_sweep(int precision, const double* R, int nr, const double* S, int ns, int d,
-              const double* scal, const double* pot, double out_scale, double out_shift,
-              double* out, double* bary, const int* gate, void* ws, size_t ws_bytes,
-              cudaStream_t st);
+              const double* scal, const double* pot, const double* row_est, double row_logw,
+              double out_scale, double out_shift, double* out, double* bary, const int* gate,
+              void* ws, size_t ws_bytes, cudaStream_t st);
 size_t ot_ws_bytes(int mode, int precision, int n, int m, int d);
 
 constexpr int SH_BLOCK = 256;
@@ -510,11 +510,12 @@ FCB_API size_t fcb_lse_sweep_workspace_bytes(int precision, int nr, int ns, int 
 }
 
 FCB_API int fcb_lse_sweep(int precision, const double* R, int nr, const double* S, int ns, int d,
-                          const double* scal, const double* pot, double out_scale,
-                          double out_shift, double* out, double* bary, const int* gate, void* ws,
-                          size_t ws_bytes, fcb_stream_t stream) {
-    return lse_sweep(precision, R, nr, S, ns, d, scal, pot, out_scale, out_shift, out, bary, gate,
-                     ws, ws_bytes, CS(stream));
+                          const double* scal, const double* pot, const double* row_est,
+                          double row_logw, double out_scale, double out_shift, double* out,
+                          double* bary, const int* gate, void* ws, size_t ws_bytes,
+                          fcb_stream_t stream) {
+    return lse_sweep(precision, R, nr, S, ns, d, scal, pot, row_est, row_logw, out_scale,
+                     out_shift, out, bary, gate, ws, ws_bytes, CS(stream));
 }
 
 FCB_API int fcb_shard_init(int precision, const double* X, int n, int d, const double* ysum,

@@ -48,6 +48,9 @@ namespace fcb {
 #ifndef FCB_MINB
 #define FCB_MINB 2       // min resident CTAs per SM (register budget)
 #endif
+#ifndef FCB_OT_SCALAR
+#define FCB_OT_SCALAR 0  // 1: fp32 sweeps use the scalar (careful) loop only
+#endif
 
 constexpr int OT_BLOCK = 256;
 constexpr int OT_SUB = 8;       // columns per register sub-tile
@@ -88,7 +91,7 @@ struct OtArgs {
     Real* pa2;
     Sweep A, B;
     GridBarrier* bar;
-    unsigned long long* errslot;  // 3 slots
+    unsigned long long* errslot;  // 3 slots + [3]: tag of the g left in gbuf (ASYM)
     double* f_out;
     double* g_out;
     double* rs_out;
@@ -99,6 +102,9 @@ struct OtArgs {
     // when epi_scale != 0, else L; bary_L stores L (not 1) in bary[i][0]
     double epi_scale, epi_shift;
     int bary_L;
+    // SWEEP-mode row shift estimate (nullable): L_i ~ row_logw - row_est_i / omega
+    const double* row_est;
+    double row_logw;
 };
 
 // ---------------------------------------------------------------------------
@@ -220,8 +226,11 @@ struct ShiftEst {
     double logw;        // log a (rows X) or log b (rows Y)
     double inv_w;       // 1 / omega
     double unit;        // exponent units per natural unit
+    int trust = 0;      // 1: close enough for the fp32 fast path (not a cold first sweep)
     __device__ __forceinline__ double at(int i) const {
-        return pot ? unit * (logw - __ldcg(pot + i) * inv_w) : 0.0;
+        if (!pot) return 0.0;
+        const double v = unit * (logw - __ldcg(pot + i) * inv_w);
+        return isfinite(v) ? v : 0.0;  // a stale/garbage estimate only costs speed
     }
 };
 
@@ -396,6 +405,123 @@ __device__ __forceinline__ void sweep_item(const Vec4<Real>* __restrict__ rows, 
     }
 }
 
+// fp32 fast path of one work item: columns staged structure-of-arrays
+// (w | q0 | q1 | q2 as float4 quads), two columns per packed FADD2/FFMA2,
+// one MUFU.EX2 per pair, no per-sub-tile range tests.  The row shift comes
+// from the potential estimate, which keeps the terms near 2^0; a row whose
+// partial sum ends outside [2^-64, 2^120] (nothing accumulated under a too-high
+// shift, overflow, NaN: the first sweep of a cold solve) makes the whole CTA
+// redo the item with the careful scalar loop (returns false).  ~5 issue slots
+// per pair with barycentres, ~3.5 without: MUFU-bound, where the scalar loop
+// (~9.6) was issue-bound.
+__device__ __forceinline__ bool f32_out_of_range(float s) {
+    constexpr unsigned LO = 0x1F800000u;  // 2^-64
+    constexpr unsigned HI = 0x7B800000u;  // 2^120
+    return (__float_as_uint(s) - LO) > (HI - LO);
+}
+
+template <int D, int RPT, bool BARY, class Cols>
+__device__ __forceinline__ bool sweep_item_f32(const Vec4<float>* __restrict__ rows, int nrows,
+                                               int row0, const Cols& cols, int c0, int c1,
+                                               float* __restrict__ soa, const ShiftEst& est,
+                                               double* __restrict__ pm, float* __restrict__ ps,
+                                               float* __restrict__ pa, int ldp, int chunk) {
+    const int tid = threadIdx.x;
+    float x[RPT][D], rc[RPT];
+    double rowc_d[RPT];
+    float2 s2[RPT], acc[RPT][D];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int i = min(row0 + r * OT_BLOCK + tid, nrows - 1);
+        const float* rp = reinterpret_cast<const float*>(rows + i);
+        const float4 v = make_float4(__ldcg(rp), __ldcg(rp + 1), __ldcg(rp + 2), __ldcg(rp + 3));
+        const float xv[3] = {v.x, v.y, v.z};
+#pragma unroll
+        for (int q = 0; q < D; ++q) x[r][q] = xv[q];
+        rowc_d[r] = (double)v.w;
+        rc[r] = (float)(rowc_d[r] - est.at(i));
+        s2[r] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < D; ++q) acc[r][q] = make_float2(0.f, 0.f);
+    }
+    const float4* wv = reinterpret_cast<const float4*>(soa);
+    const float4* qv[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) qv[q] = reinterpret_cast<const float4*>(soa + (q + 1) * FCB_TILE);
+    for (int t0 = c0; t0 < c1; t0 += FCB_TILE) {
+        const int tlen = min(FCB_TILE, c1 - t0);
+        __syncthreads();
+        for (int k = tid; k < tlen; k += OT_BLOCK) {
+            const Vec4<float> c = cols(t0 + k);
+            soa[k] = c.w;
+            soa[FCB_TILE + k] = c.x;
+            if (D > 1) soa[2 * FCB_TILE + k] = c.y;
+            if (D > 2) soa[3 * FCB_TILE + k] = c.z;
+        }
+        __syncthreads();
+        for (int c = 0; c < tlen; c += OT_SUB) {
+            const int q0 = c >> 2, q1 = q0 + 1;
+            float w[8], y[D][8];
+            {
+                const float4 a = wv[q0], b = wv[q1];
+                w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+                w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+            }
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                const float4 a = qv[q][q0], b = qv[q][q1];
+                y[q][0] = a.x; y[q][1] = a.y; y[q][2] = a.z; y[q][3] = a.w;
+                y[q][4] = b.x; y[q][5] = b.y; y[q][6] = b.z; y[q][7] = b.w;
+            }
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const float2 rc2 = make_float2(rc[r], rc[r]);
+                float2 e[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    float2 t = __fadd2_rn(make_float2(w[2 * u], w[2 * u + 1]), rc2);
+#pragma unroll
+                    for (int q = 0; q < D; ++q)
+                        t = __ffma2_rn(make_float2(x[r][q], x[r][q]),
+                                       make_float2(y[q][2 * u], y[q][2 * u + 1]), t);
+                    e[u] = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+                }
+                s2[r] = __fadd2_rn(s2[r], __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3])));
+                if constexpr (BARY) {
+#pragma unroll
+                    for (int q = 0; q < D; ++q)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            acc[r][q] = __ffma2_rn(e[u], make_float2(y[q][2 * u], y[q][2 * u + 1]),
+                                                   acc[r][q]);
+                }
+            }
+        }
+    }
+    bool bad = false;
+    float sum[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        sum[r] = s2[r].x + s2[r].y;
+        if (row0 + r * OT_BLOCK + tid < nrows) bad |= f32_out_of_range(sum[r]);
+    }
+    if (__syncthreads_or(bad)) return false;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int i = row0 + r * OT_BLOCK + tid;
+        if (i < nrows) {
+            pm[(size_t)chunk * ldp + i] = rowc_d[r] - (double)rc[r];
+            ps[(size_t)chunk * ldp + i] = sum[r];
+            if constexpr (BARY) {
+#pragma unroll
+                for (int q = 0; q < D; ++q)
+                    pa[((size_t)chunk * D + q) * ldp + i] = acc[r][q].x + acc[r][q].y;
+            }
+        }
+    }
+    return true;
+}
+
 // All items of a sweep.  Item blockIdx.x is static (no atomic before the
 // first item); the rest are handed out dynamically, so CTAs that run faster
 // (an SM shared with a slower neighbour, earlier start) take more items.  The
@@ -419,8 +545,17 @@ __device__ __forceinline__ void run_sweep(const Sweep& sw, const Vec4<Real>* row
         const int ch = item / sw.nrb;
         const int c0 = ch * sw.chunk_len;
         const int c1 = min(c0 + sw.chunk_len, sw.cols8);
-        sweep_item<Real, D, RPT, EXP, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT, cols.for_block(rb),
-                                            c0, c1, s_tile, s, est, pm, ps, pa, ldp, ch);
+        bool done = false;
+        if constexpr (EXP && sizeof(Real) == 4 && !FCB_OT_SCALAR) {
+            if (est.trust) done = sweep_item_f32<D, RPT, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT,
+                                                cols.for_block(rb), c0, c1,
+                                                reinterpret_cast<float*>(s_tile), est, pm, ps, pa,
+                                                ldp, ch);
+        }
+        if (!done)
+            sweep_item<Real, D, RPT, EXP, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT,
+                                                cols.for_block(rb), c0, c1, s_tile, s, est, pm, ps,
+                                                pa, ldp, ch);
         __syncthreads();
         if (threadIdx.x == 0) s_item = grid + (int)(nxt - base);
         __syncthreads();
@@ -609,8 +744,8 @@ __device__ __forceinline__ void sweep_only_pass(const OtArgs<Real>& p, const OtS
     const double* c = sc.c;
     const double csc = EXP ? 2.0 * sc.sd : 1.0;
     const double unit = Units<Real>::unit;
-    const ShiftEst none{nullptr, 0.0, 0.0, unit};
-    run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colY}, s, none, p.pm, p.ps,
+    const ShiftEst est{p.row_est, p.row_logw, 1.0 / sc.w, unit, p.row_est != nullptr};
+    run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colY}, s, est, p.pm, p.ps,
                                        p.pa, &p.bar->work, 0u, s_tile);
     grid_sync(p.bar);
     double* out = p.f_out;
@@ -625,12 +760,16 @@ __device__ __forceinline__ void sweep_only_pass(const OtArgs<Real>& p, const OtS
     });
 }
 
+__device__ __forceinline__ unsigned long long gbuf_tag(int m) {
+    return 0x5EEDF10C00000000ull ^ (unsigned long long)(unsigned)m;
+}
+
 // The Sinkhorn iterations of an ASYM or SYM solve (after pack_phase and a
 // grid barrier) up to convergence or max_iters, then the outputs.  wbase:
 // work-counter base, carried across solves that share the barrier.
 template <typename Real, int D, int RPT, bool BARY>
 __device__ __forceinline__ void solve_loop(const OtArgs<Real>& p, const OtScal& sc, unsigned& wbase,
-                                           double* red, Vec4<Real>* s_tile) {
+                                           double* red, Vec4<Real>* s_tile, bool warm) {
     constexpr bool EXP = (sizeof(Real) == 4);
     const double w = sc.w;
     const double sd = sc.sd;
@@ -654,11 +793,18 @@ __device__ __forceinline__ void solve_loop(const OtArgs<Real>& p, const OtScal& 
         double* pmB = asym ? p.pm2 : p.pm;
         Real* psB = asym ? p.ps2 : p.ps;
         Real* paB = asym ? p.pa2 : p.pa;
-        const ShiftEst estB{fcur, p.loga, 1.0 / w, unit};
+        // the first sweep of a cold solve shifts by an estimate from f = 0:
+        // it takes the careful loop directly
+        const ShiftEst estB{fcur, p.loga, 1.0 / w, unit, (it > 1 || warm) ? 1 : 0};
         if (asym) {
             // ---- sweep A: rows Y, columns X (potential f) --------------
-            // shift estimate: g of the previous iteration (none at it == 1)
-            const ShiftEst estA{it > 1 ? p.gbuf : nullptr, p.logb, 1.0 / w, unit};
+            // shift estimate: g of the previous iteration; at it == 1 of a
+            // warm-started solve, the g the previous solve on this workspace
+            // left behind (tagged with m) -- the estimate only shifts the terms
+            // (rounding), never the math; cold solves never use it, so a
+            // repeated cold call stays bit-identical
+            const bool gprev = it > 1 || (warm && __ldcg(p.errslot + 3) == gbuf_tag(p.m));
+            const ShiftEst estA{gprev ? p.gbuf : nullptr, p.logb, 1.0 / w, unit, gprev ? 1 : 0};
             run_sweep<Real, D, RPT, EXP, false>(p.A, p.rowY, PlainCols<Real>{p.colX}, s, estA, p.pm,
                                                 p.ps, p.pa, &p.bar->work, wbase, s_tile);
             wbase += (unsigned)p.A.items;
@@ -716,6 +862,7 @@ __device__ __forceinline__ void solve_loop(const OtArgs<Real>& p, const OtScal& 
             for (int i = gtid; i < p.n; i += gthreads) p.f_out[i] = __ldcg(fcur + i);
             if (asym && p.g_out)
                 for (int j = gtid; j < p.m; j += gthreads) p.g_out[j] = __ldcg(p.gbuf + j);
+            if (asym && gtid == 0) p.errslot[3] = gbuf_tag(p.m);
             if (gtid == 0) {
                 p.stat[0] = err;
                 p.stat[1] = (double)it;
@@ -741,7 +888,7 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
         return;
     }
     unsigned wbase = 0;
-    solve_loop<Real, D, RPT, BARY>(p, sc, wbase, red, s_tile);
+    solve_loop<Real, D, RPT, BARY>(p, sc, wbase, red, s_tile, p.f0 != nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -859,8 +1006,8 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) flow_kernel(FlowArgs<Real>
     grid_sync(A.bar);
 
     unsigned wbase = 0;
-    solve_loop<Real, D, RPT, true>(A, scA, wbase, red, s_tile);
-    solve_loop<Real, D, RPT, true>(B, scB, wbase, red, s_tile);
+    solve_loop<Real, D, RPT, true>(A, scA, wbase, red, s_tile, vf);
+    solve_loop<Real, D, RPT, true>(B, scB, wbase, red, s_tile, vp);
     grid_sync(A.bar);
 
     // ---- finalize: FlowError test, envelope gradient, warm state ----------
@@ -1044,6 +1191,8 @@ static void ot_layout(OtLayout<Real>& L, int mode, int n, int m, int d, int rpt,
 struct OtEpi {
     double scale = 0.0, shift = 0.0;
     int bary_L = 0;
+    const double* row_est = nullptr;
+    double row_logw = 0.0;
 };
 
 template <typename Real, int D, int RPT, bool BARY>
@@ -1075,6 +1224,8 @@ static int ot_launch(int mode, const double* X, int n, const double* Y, int m, c
     a.epi_scale = epi.scale;
     a.epi_shift = epi.shift;
     a.bary_L = epi.bary_L;
+    a.row_est = epi.row_est;
+    a.row_logw = epi.row_logw;
     FCB_CUDA(cudaMemsetAsync(a.bar, 0, sizeof(GridBarrier), st));
     void* args[] = {&a};
     FCB_CUDA(cudaLaunchCooperativeKernel((const void*)ot_solve_kernel<Real, D, RPT, BARY>,
@@ -1103,7 +1254,10 @@ static int ot_dispatch(int mode, int d, const double* X, int n, const double* Y,
     return fail(FCB_ENOTSUP, "point dimension must be 1, 2 or 3");
 }
 
-constexpr int RPT_F32 = 2;
+#ifndef FCB_RPT32
+#define FCB_RPT32 3  // measured at config 4: 3 > 2 (+7 % solve), 4 spills or halves occupancy
+#endif
+constexpr int RPT_F32 = FCB_RPT32;  // rows per thread of the fp32 sweeps
 constexpr int RPT_F64 = 1;
 
 template <typename Real, int RPT>
@@ -1173,15 +1327,17 @@ static int lse_sweep_t(int d, const double* R, int nr, const double* S, int ns, 
 }
 
 int lse_sweep(int precision, const double* R, int nr, const double* S, int ns, int d,
-              const double* scal, const double* pot, double out_scale, double out_shift,
-              double* out, double* bary, const int* gate, void* ws, size_t ws_bytes,
-              cudaStream_t st) {
+              const double* scal, const double* pot, const double* row_est, double row_logw,
+              double out_scale, double out_shift, double* out, double* bary, const int* gate,
+              void* ws, size_t ws_bytes, cudaStream_t st) {
     if (nr < 1 || ns < 1) return fail(FCB_EINPUT, "empty point set");
     if (!pot) return fail(FCB_EINPUT, "sweep needs a potential");
     OtEpi epi;
     epi.scale = out_scale;
     epi.shift = out_shift;
     epi.bary_L = 1;
+    epi.row_est = row_est;
+    epi.row_logw = row_logw;
     if (precision == FCB_FP64)
         return lse_sweep_t<double, RPT_F64>(d, R, nr, S, ns, scal, pot, out, bary, gate, ws,
                                             ws_bytes, st, epi);

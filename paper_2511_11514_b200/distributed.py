@@ -124,13 +124,15 @@ class DeviceOps:
     def workspace(self, nbytes: int, tag: str) -> torch.Tensor:
         return _dev.Workspace.get(nbytes, tag)
 
-    def lse_sweep(self, prec, R, S, scal, pot, scale, shift, out, bary, gate, tag):
+    def lse_sweep(self, prec, R, S, scal, pot, scale, shift, out, bary, gate, tag,
+                  est=None, est_logw=0.0):
         nr, d = R.shape
         ns = S.shape[0]
         ws = self.workspace(self.lib.fcb_lse_sweep_workspace_bytes(prec, nr, ns, d), tag)
         self._call("fcb_lse_sweep", prec, _dev.ptr(R), nr, _dev.ptr(S), ns, d, _dev.ptr(scal),
-                   _dev.ptr(pot), float(scale), float(shift), _dev.ptr(out), _dev.ptr(bary),
-                   _dev.ptr(gate), _dev.ptr(ws), ws.numel(), _dev.stream())
+                   _dev.ptr(pot), _dev.ptr(est), float(est_logw), float(scale), float(shift),
+                   _dev.ptr(out), _dev.ptr(bary), _dev.ptr(gate), _dev.ptr(ws), ws.numel(),
+                   _dev.stream())
 
     def shard_init(self, prec, X, ysum, omega_fixed, warm_f, warm_p, warm_valid, scal_x, scal_s,
                    f, p, ctl, eslot, plan_state):
@@ -259,6 +261,8 @@ class ShardedSinkhorn:
         self.prec = (precision if precision is not None else
                      _precision.pick(cfg.precision, n * max(n, self.m_global), cfg.tol))
         self.logb = -math.log(self.m_global)
+        self.loga = -math.log(n)
+        self.log_frac = math.log(max(m_r, 1) / self.m_global)
         self.rows = shard_bounds(n, rank, R)
         self.nown = self.rows[1] - self.rows[0]
         self.chunk = (n + R - 1) // R
@@ -283,12 +287,13 @@ class ShardedSinkhorn:
     def _cross_iteration(self, X):
         ops, cfg, d = self.ops, self.cfg, self.d
         gate = self.ctl[0:1]
-        # g_r = w (log b - LSE_rows(Y_r vs X; f))
+        # g_r = w (log b - LSE_rows(Y_r vs X; f)); rows shifted by the last g
         ops.lse_sweep(self.prec, self.Y, X, self.scal_x, self.f, 1.0, self.logb, self.g, None,
-                      gate, "shard_sw")
-        # {L_r, ybar_r} of rows X vs Y_r under g_r, gathered over ranks
+                      gate, "shard_sw", est=self.g, est_logw=self.logb)
+        # {L_r, ybar_r} of rows X vs Y_r under g_r, gathered over ranks; the
+        # shard's LSE is ~ log(m_r / M) below the full one, log a - f / w
         ops.lse_sweep(self.prec, X, self.Y, self.scal_x, self.g, 0.0, 0.0, None, self.send_x,
-                      gate, "shard_sw")
+                      gate, "shard_sw", est=self.f, est_logw=self.loga + self.log_frac)
         self.coll.all_gather(self.gath_x, self.send_x)
         ops.cross_merge(self.n, d, self.coll.world, self.gath_x, self.scal_x, cfg.tol,
                         cfg.max_iters, self.f, self.fnext, self.rs, self.mass, self.ybar,
@@ -300,7 +305,7 @@ class ShardedSinkhorn:
         lo, hi = self.rows
         if self.nown > 0:
             ops.lse_sweep(self.prec, X[lo:hi], X, self.scal_s, self.p, 0.0, 0.0, None, self.Lb,
-                          gate, "shard_sw")
+                          gate, "shard_sw", est=self.p[lo:hi], est_logw=self.loga)
             ops.self_rows(self.n, d, lo, self.nown, self.Lb, self.scal_s, self.p, self.send_s,
                           self.ctl)
         self.coll.all_gather(self.gath_s, self.send_s)

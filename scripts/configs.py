@@ -1,6 +1,9 @@
 """Measure BASELINE.json configs beyond the bench workload (one GPU).
 
-    python scripts/configs.py [cfg ...]      cfg in {1, 3, 4, 4s, 5}
+    python scripts/configs.py [cfg ...]      cfg in {1, 3, 4, 4s, 5, 5full}
+
+5full: all 4096 config-5 problems in one batched launch on one GPU (the
+8-GPU split runs 512 per rank through distributed.plan_batch).
 
 Every config prints one JSON line: outer iterations timed, planner it/s,
 executed pair evaluations per second over the whole planner step, and (for
@@ -194,7 +197,8 @@ def cfg5(problems=512, iters=100):
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["1", "3", "4", "4s", "5"]
-    table = {"1": cfg1, "3": cfg3, "4": cfg4, "4s": cfg4s, "5": cfg5}
+    table = {"1": cfg1, "3": cfg3, "4": cfg4, "4s": cfg4s, "5": cfg5,
+             "5full": lambda: cfg5(problems=4096)}
     for w in which:
         res = table[w]()
         print(json.dumps(res), flush=True)

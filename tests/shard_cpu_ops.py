@@ -47,7 +47,8 @@ class CpuOps:
         out[d] = (P * P).sum()
         out[d + 1] = float(P.shape[0])
 
-    def lse_sweep(self, prec, R, S, scal, pot, scale, shift, out, bary, gate, tag):
+    def lse_sweep(self, prec, R, S, scal, pot, scale, shift, out, bary, gate, tag, est=None,
+                  est_logw=0.0):
         if gate is not None and int(gate[0]) != 0:
             return
         w = float(scal[0])
