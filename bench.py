@@ -283,8 +283,8 @@ def run_ours(args):
     roof = {
         "bound": "mufu/fp32 (co-limited; composite of SURVEY.md 8(d) per-sweep roofs)",
         "kernel": ("flow_kernel<float,3,3> (chunked fp32 Sinkhorn flow, cross + self solves) + "
-                   "sv_sweep_kernel<float,3,2> (SVGD)" if world == 1 else
-                   "sharded lse sweeps (ot_solve_kernel SWEEP mode) + sv_sweep_kernel"),
+                   "sv_sweep_f32_kernel<3,4> (packed SVGD)" if world == 1 else
+                   "sharded lse sweeps (ot_solve_kernel SWEEP mode) + sv_sweep_f32_kernel"),
         "achieved": fpairs / t_flow / 1e9,
         "peak": fpairs / t_roof / 1e9,
         "unit": "Gpair/s",

@@ -43,11 +43,16 @@ class PlannerRun:
     t_rollout: float
 
 
-def b200_planners(spec: Any, planner_run: Callable[..., Any] | None = None) -> dict[str, Callable]:
+def b200_planners(spec: Any, planner_run: Callable[..., Any] | None = None,
+                  reference_names: bool = False) -> dict[str, Callable]:
     """Planner closures for a reference BenchSpec (duck-typed: model, dt, seed, plan).
 
     planner_run: the harness's PlannerRun class (defaults to this module's
     mirror), so the rows it writes are the reference's own type.
+    reference_names: key the closures "stein" / "sinkhorn" -- the method names
+    BenchSpec validates (bench.py:67-69) -- so `run_bench(spec, planners=...)`
+    times the device planners under the stock spec; default keys are
+    "b200-stein" / "b200-sinkhorn" for merging into standard_planners().
     """
     make_run = planner_run or PlannerRun
     model = get_model(spec.model)
@@ -72,4 +77,5 @@ def b200_planners(spec: Any, planner_run: Callable[..., Any] | None = None) -> d
 
         return run
 
-    return {"b200-stein": flow_planner("stein"), "b200-sinkhorn": flow_planner("sinkhorn")}
+    prefix = "" if reference_names else "b200-"
+    return {f"{prefix}stein": flow_planner("stein"), f"{prefix}sinkhorn": flow_planner("sinkhorn")}

@@ -48,6 +48,9 @@ namespace fcb {
 #ifndef FCB_MINB
 #define FCB_MINB 2       // min resident CTAs per SM (register budget)
 #endif
+#ifndef FCB_SAMPLE
+#define FCB_SAMPLE 32    // sampled columns per item for the cold-sweep row shift
+#endif
 #ifndef FCB_OT_SCALAR
 #define FCB_OT_SCALAR 0  // 1: fp32 sweeps use the scalar (careful) loop only
 #endif
@@ -444,6 +447,35 @@ __device__ __forceinline__ bool sweep_item_f32(const Vec4<float>* __restrict__ r
 #pragma unroll
         for (int q = 0; q < D; ++q) acc[r][q] = make_float2(0.f, 0.f);
     }
+    if (!est.trust) {
+        // no usable potential estimate (first sweep of a cold solve): shift
+        // each row by its max over FCB_SAMPLE columns spread over this item's
+        // chunk -- the partial sum is then >= 1; only a chunk whose best
+        // column beats the sample's by > ~2^100 falls back to the careful loop
+        constexpr int NS = FCB_SAMPLE;
+        __syncthreads();
+        if (tid < NS) {
+            const int span = c1 - c0;
+            const Vec4<float> c = cols(c0 + (int)(((long long)span * tid) / NS));
+            soa[tid] = c.w;
+            soa[NS + tid] = c.x;
+            soa[2 * NS + tid] = c.y;
+            soa[3 * NS + tid] = c.z;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            float mx = -INFINITY;
+            for (int k = 0; k < NS; ++k) {
+                float t = soa[k] + (float)rowc_d[r];
+                t = fmaf(x[r][0], soa[NS + k], t);
+                if (D > 1) t = fmaf(x[r][1], soa[2 * NS + k], t);
+                if (D > 2) t = fmaf(x[r][2], soa[3 * NS + k], t);
+                mx = fmaxf(mx, t);
+            }
+            if (mx > -INFINITY && mx < INFINITY) rc[r] = (float)(rowc_d[r] - (double)mx);
+        }
+    }
     const float4* wv = reinterpret_cast<const float4*>(soa);
     const float4* qv[D];
 #pragma unroll
@@ -547,7 +579,7 @@ __device__ __forceinline__ void run_sweep(const Sweep& sw, const Vec4<Real>* row
         const int c1 = min(c0 + sw.chunk_len, sw.cols8);
         bool done = false;
         if constexpr (EXP && sizeof(Real) == 4 && !FCB_OT_SCALAR) {
-            if (est.trust) done = sweep_item_f32<D, RPT, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT,
+            done = sweep_item_f32<D, RPT, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT,
                                                 cols.for_block(rb), c0, c1,
                                                 reinterpret_cast<float*>(s_tile), est, pm, ps, pa,
                                                 ldp, ch);

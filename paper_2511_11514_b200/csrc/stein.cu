@@ -346,6 +346,9 @@ constexpr int SV_BLOCK = 256;
 constexpr int SV_TILE = 256;
 constexpr int SV_SUB = 8;
 constexpr int SV_MAXCH = 64;
+#ifndef FCB_SV_SCALAR
+#define FCB_SV_SCALAR 0  // 1: fp32 SVGD sweeps use the scalar loop
+#endif
 
 template <typename Real>
 struct alignas(sizeof(Real) * 4) SvCol {
@@ -487,6 +490,113 @@ __global__ void __launch_bounds__(SV_BLOCK) sv_sweep_kernel(SvPlan pl,
     }
 }
 
+// fp32 sweep with packed FADD2/FFMA2: columns staged structure-of-arrays
+// (-x~_j and w_j per coordinate, float4 quads), two columns per packed op, the
+// direct form k = 2^-(|x~_i - x~_j|^2) with the negation folded into the
+// MUFU.EX2 operand.  ~6 issue slots per pair (scalar loop: ~11).
+template <int D, int RPT>
+__global__ void __launch_bounds__(SV_BLOCK) sv_sweep_f32_kernel(SvPlan pl,
+                                                                const Vec4<float>* __restrict__ rows,
+                                                                const SvCol<float>* __restrict__ cols,
+                                                                float* __restrict__ part,
+                                                                const int* gate) {
+    __shared__ __align__(16) float s_y[D][SV_TILE];
+    __shared__ __align__(16) float s_w[D][SV_TILE];
+    if (gate && *((volatile const int*)gate) != 0) return;
+    const int n = pl.n;
+    for (int item = blockIdx.x; item < pl.items; item += gridDim.x) {
+        const int rb = item % pl.nrb, ch = item / pl.nrb;
+        const int c0 = ch * pl.chunk_len, c1 = min(c0 + pl.chunk_len, pl.n8);
+        const int row0 = rb * SV_BLOCK * RPT;
+        float2 x2[RPT][D], ks2[RPT], acc2[RPT][D];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int i = min(row0 + r * SV_BLOCK + threadIdx.x, n - 1);
+            const Vec4<float> v = rows[i];
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                const float xv = vget(v, q);
+                x2[r][q] = make_float2(xv, xv);
+                acc2[r][q] = make_float2(0.f, 0.f);
+            }
+            ks2[r] = make_float2(0.f, 0.f);
+        }
+        for (int t0 = c0; t0 < c1; t0 += SV_TILE) {
+            const int len = min(SV_TILE, c1 - t0);
+            __syncthreads();
+            for (int k = threadIdx.x; k < len; k += SV_BLOCK) {
+                const SvCol<float> c = cols[t0 + k];
+#pragma unroll
+                for (int q = 0; q < D; ++q) {
+                    s_y[q][k] = -c.x[q];
+                    s_w[q][k] = c.w[q];
+                }
+            }
+            __syncthreads();
+            for (int c = 0; c < len; c += SV_SUB) {
+                float y[D][8], w[D][8];
+#pragma unroll
+                for (int q = 0; q < D; ++q) {
+                    const float4 a = *reinterpret_cast<const float4*>(&s_y[q][c]);
+                    const float4 b = *reinterpret_cast<const float4*>(&s_y[q][c + 4]);
+                    y[q][0] = a.x; y[q][1] = a.y; y[q][2] = a.z; y[q][3] = a.w;
+                    y[q][4] = b.x; y[q][5] = b.y; y[q][6] = b.z; y[q][7] = b.w;
+                    const float4 e = *reinterpret_cast<const float4*>(&s_w[q][c]);
+                    const float4 f = *reinterpret_cast<const float4*>(&s_w[q][c + 4]);
+                    w[q][0] = e.x; w[q][1] = e.y; w[q][2] = e.z; w[q][3] = e.w;
+                    w[q][4] = f.x; w[q][5] = f.y; w[q][6] = f.z; w[q][7] = f.w;
+                }
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    float2 e[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float2 d2 = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int q = 0; q < D; ++q) {
+                            const float2 df = __fadd2_rn(x2[r][q], make_float2(y[q][2 * u], y[q][2 * u + 1]));
+                            d2 = __ffma2_rn(df, df, d2);
+                        }
+                        e[u] = make_float2(ex2_approx(-d2.x), ex2_approx(-d2.y));
+                    }
+                    ks2[r] = __fadd2_rn(ks2[r], __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3])));
+#pragma unroll
+                    for (int q = 0; q < D; ++q)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            acc2[r][q] = __ffma2_rn(e[u], make_float2(w[q][2 * u], w[q][2 * u + 1]),
+                                                    acc2[r][q]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int i = row0 + r * SV_BLOCK + threadIdx.x;
+            if (i < n) {
+                part[((size_t)ch * (D + 1)) * n + i] = ks2[r].x + ks2[r].y;
+#pragma unroll
+                for (int q = 0; q < D; ++q)
+                    part[((size_t)ch * (D + 1) + 1 + q) * n + i] = acc2[r][q].x + acc2[r][q].y;
+            }
+        }
+    }
+}
+
+// Launch the sweep of the precision (fp32: the packed kernel).
+template <typename Real, int D, int RPT>
+static void sv_sweep_launch(const SvPlan& pl, int grid, const void* rows, const void* cols,
+                            void* part, const int* gate, cudaStream_t st) {
+    if constexpr (sizeof(Real) == 4 && !FCB_SV_SCALAR) {
+        sv_sweep_f32_kernel<D, RPT><<<grid, SV_BLOCK, 0, st>>>(
+            pl, static_cast<const Vec4<float>*>(rows), static_cast<const SvCol<float>*>(cols),
+            static_cast<float*>(part), gate);
+    } else {
+        sv_sweep_kernel<Real, D, RPT><<<grid, SV_BLOCK, 0, st>>>(
+            pl, static_cast<const Vec4<Real>*>(rows), static_cast<const SvCol<Real>*>(cols),
+            static_cast<Real*>(part), gate);
+    }
+}
+
 template <typename Real, int D>
 __global__ void sv_merge_kernel(SvPlan pl, const Real* __restrict__ part,
                                 const double* __restrict__ X, const double* __restrict__ hstat,
@@ -513,7 +623,7 @@ __global__ void sv_merge_kernel(SvPlan pl, const Real* __restrict__ part,
     }
 }
 
-constexpr int SV_RPT_F32 = 2;
+constexpr int SV_RPT_F32 = 4;  // packed loop: 4 rows per thread halve the shared-memory loads per pair
 constexpr int SV_RPT_F64 = 1;
 
 // Sharded sources (fcb_stein_partial): query rows are all n points, source
@@ -625,9 +735,7 @@ static int stein_run(const double* X, int n, const double* scores, const double*
                                                static_cast<Vec4<Real>*>(L.rows), gate);
     FCB_LAUNCHED("sv_pack_kernel");
     const int grid = std::min(pl.items, sv_grid());
-    sv_sweep_kernel<Real, D, RPT><<<grid, SV_BLOCK, 0, st>>>(
-        pl, static_cast<const Vec4<Real>*>(L.rows), static_cast<const SvCol<Real>*>(L.cols),
-        static_cast<Real*>(L.part), gate);
+    sv_sweep_launch<Real, D, RPT>(pl, grid, L.rows, L.cols, L.part, gate, st);
     FCB_LAUNCHED("sv_sweep_kernel");
     const int mb = std::max(1, std::min(4 * sm_count(), (n + 255) / 256));
     sv_merge_kernel<Real, D><<<mb, 256, 0, st>>>(pl, static_cast<const Real*>(L.part), X, hstat,
@@ -675,9 +783,7 @@ static int stein_partial_run(const double* X, int n, int col0, int nc, const dou
                                                      static_cast<Vec4<Real>*>(L.rows), gate);
     FCB_LAUNCHED("sv_pack_range_kernel");
     const int grid = std::min(pl.items, sv_grid());
-    sv_sweep_kernel<Real, D, RPT><<<grid, SV_BLOCK, 0, st>>>(
-        pl, static_cast<const Vec4<Real>*>(L.rows), static_cast<const SvCol<Real>*>(L.cols),
-        static_cast<Real*>(L.part), gate);
+    sv_sweep_launch<Real, D, RPT>(pl, grid, L.rows, L.cols, L.part, gate, st);
     FCB_LAUNCHED("sv_sweep_kernel");
     const int mb = std::max(1, std::min(4 * sm_count(), (n + 255) / 256));
     sv_merge_raw_kernel<Real, D><<<mb, 256, 0, st>>>(pl, static_cast<const Real*>(L.part), out,
