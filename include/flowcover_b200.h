@@ -160,6 +160,13 @@ FCB_API int fcb_sinkhorn_divergence(int precision, const double* X, int n, const
 FCB_API int fcb_gmm_eval(const double* X, int n, int d, int k, const double* params, double* score,
                  double* logdens, const int* gate, fcb_stream_t stream);
 
+/* SamplePoints.sample (reference.py:140-146) on a device-resident cloud:
+ * out (n*d) = src rows idx[0..n) (host-drawn PCG64 indices, int32, uploaded);
+ * status (nullable device int): -1, or the first position with an index
+ * outside [0, m). */
+FCB_API int fcb_gather_rows(const double* src, int m, int d, const int* idx, int n, double* out,
+                            int* status, fcb_stream_t stream);
+
 /* ---- Stein variational flow (stein.py) ---------------------------------- */
 
 /* median_bandwidth (stein.py:66-76): exact np.median over all n^2 pairwise
@@ -344,11 +351,39 @@ FCB_API size_t fcb_stein_partial_workspace_bytes(int precision, int n, int nc, i
 FCB_API int fcb_stein_partial(int precision, const double* X, int n, int d, int col0, int ncols,
                               const double* scores, const double* hstat, double* part,
                               const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream);
+/* median_bandwidth (stein.py:66-76) with the pair tiles split across ranks:
+ * init; then for pass = 0..5: fcb_median_shard_pass over this rank's tiles
+ * [tile_lo, tile_hi) of the fcb_median_tiles(n) upper-triangle tiles, an
+ * all_reduce(SUM) of the 2 x 2048 uint64 histogram at byte offset
+ * fcb_median_hist_offset() of ws, fcb_median_shard_select (every rank picks
+ * the same digit); then fcb_median_shard_finish writes hstat as
+ * fcb_median_bandwidth does.  ws: fcb_median_workspace_bytes(n). */
+FCB_API long long fcb_median_tiles(int n);
+FCB_API size_t fcb_median_hist_offset(void);
+FCB_API int fcb_median_shard_init(int n, void* ws, size_t ws_bytes, const int* gate,
+                                  fcb_stream_t stream);
+FCB_API int fcb_median_shard_pass(const double* X, int n, int d, int pass, long long tile_lo,
+                                  long long tile_hi, void* ws, const int* gate,
+                                  fcb_stream_t stream);
+FCB_API int fcb_median_shard_select(int n, int pass, void* ws, const int* gate,
+                                    fcb_stream_t stream);
+FCB_API int fcb_median_shard_finish(int n, double log_np1, double* hstat, void* ws,
+                                    const int* gate, fcb_stream_t stream);
 FCB_API size_t fcb_stein_combine_workspace_bytes(int n);
 FCB_API int fcb_stein_combine(const double* X, int n, int d, int R, const double* parts,
                               const double* hstat, double* flow, double* fstat, int* plan_state,
                               int iteration, double* flow_log, double conv_tol, void* ws,
                               size_t ws_bytes, fcb_stream_t stream);
+
+/* ---- TSP-waypoint baseline (tsp.py) ---------------------------------------
+ * build_tour (tsp.py:120-147) for `batch` independent point sets of n points
+ * (points: batch*n*d, row-major per problem), one CTA each: nearest-neighbour
+ * order from starts[b] (drawn on the host from stream [seed, 4]) refined by
+ * first-improving 2-opt moves (tsp.py:92-117) until none improves or `budget`
+ * moves were made.  order: batch*n out (int32); moves: batch out (nullable).
+ * Same arithmetic as the reference, so the orders are identical. */
+FCB_API int fcb_tsp_tours(const double* points, int batch, int n, int d, const int* starts,
+                          int budget, int* order, int* moves, fcb_stream_t stream);
 
 /* ---- measurement helpers ------------------------------------------------- */
 

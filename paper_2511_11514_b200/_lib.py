@@ -74,6 +74,7 @@ SIGNATURES: dict[str, tuple] = {
     "fcb_sinkhorn_divergence_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "fcb_sinkhorn_divergence": (_I, [_I, _P, _I, _P, _I, _I, _D, _I, _D, _P, _P, _P, _Z, _P]),
     "fcb_gmm_eval": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "fcb_gather_rows": (_I, [_P, _I, _I, _P, _I, _P, _P, _P]),
     "fcb_median_workspace_bytes": (_Z, [_I]),
     "fcb_median_bandwidth": (_I, [_P, _I, _I, _D, _P, _P, _P, _Z, _P]),
     "fcb_stein_workspace_bytes": (_Z, [_I, _I, _I]),
@@ -121,8 +122,16 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "fcb_stein_partial_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "fcb_stein_partial": (_I, [_I, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _Z, _P]),
+    "fcb_median_tiles": (ctypes.c_longlong, [_I]),
+    "fcb_median_hist_offset": (_Z, []),
+    "fcb_median_shard_init": (_I, [_I, _P, _Z, _P, _P]),
+    "fcb_median_shard_pass": (_I, [_P, _I, _I, _I, ctypes.c_longlong,
+                                   ctypes.c_longlong, _P, _P, _P]),
+    "fcb_median_shard_select": (_I, [_I, _I, _P, _P, _P]),
+    "fcb_median_shard_finish": (_I, [_I, _D, _P, _P, _P, _P]),
     "fcb_stein_combine_workspace_bytes": (_Z, [_I]),
     "fcb_stein_combine": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I, _P, _D, _P, _Z, _P]),
+    "fcb_tsp_tours": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _P]),
     "fcb_peak_probe": (_I, [_I, _I, _P, _P]),
     "fcb_debug_timeline": (_I, [_P, _I]),
 }

@@ -67,6 +67,8 @@ size_t sinkhorn_divergence_ws_bytes(int precision, int n, int m, int d);
 int sinkhorn_divergence(int precision, const double* X, int n, const double* Y, int m, int d,
                         double omega_fixed, int max_iters, double tol, double* out,
                         const int* gate, void* ws, size_t ws_bytes, cudaStream_t st);
+int gather_rows(const double* src, int m, int d, const int* idx, int n, double* out, int* status,
+                cudaStream_t st);
 int gmm_eval(const double* X, int n, int d, int k, const double* prm, double* score,
              double* logdens, const int* gate, cudaStream_t st);
 size_t median_ws_bytes(int n);
@@ -243,6 +245,11 @@ int fcb_sinkhorn_divergence(int precision, const double* X, int n, const double*
     if (n < 1 || m < 1) return fail(FCB_EINPUT, "point sets must be non-empty");
     return sinkhorn_divergence(precision, X, n, Y, m, d, omega_fixed, max_iters, tol, out, gate, ws,
                                ws_bytes, CS(stream));
+}
+
+int fcb_gather_rows(const double* src, int m, int d, const int* idx, int n, double* out,
+                    int* status, fcb_stream_t stream) {
+    return gather_rows(src, m, d, idx, n, out, status, CS(stream));
 }
 
 int fcb_gmm_eval(const double* X, int n, int d, int k, const double* params, double* score,

@@ -415,6 +415,15 @@ int stein_partial(int precision, const double* X, int n, int d, int col0, int nc
                   const double* scores, const double* hstat, double* part, const int* gate,
                   void* ws, size_t ws_bytes, cudaStream_t st);
 size_t stein_partial_ws_bytes(int precision, int n, int nc, int d);
+size_t median_ws_bytes(int n);
+long long median_tiles(int n);
+size_t median_hist_offset();
+int median_shard_init(int n, void* ws, size_t ws_bytes, const int* gate, cudaStream_t st);
+int median_shard_pass(const double* X, int n, int d, int pass, long long t_lo, long long t_hi,
+                      void* ws, const int* gate, cudaStream_t st);
+int median_shard_select(int n, int pass, void* ws, const int* gate, cudaStream_t st);
+int median_shard_finish(int n, double log_np1, double* hstat, void* ws, const int* gate,
+                        cudaStream_t st);
 
 template <int D>
 __global__ void __launch_bounds__(SH_BLOCK)
@@ -617,6 +626,30 @@ FCB_API int fcb_stein_partial(int precision, const double* X, int n, int d, int 
                               const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream) {
     return stein_partial(precision, X, n, d, col0, ncols, scores, hstat, part, gate, ws, ws_bytes,
                          CS(stream));
+}
+
+FCB_API long long fcb_median_tiles(int n) { return median_tiles(n); }
+FCB_API size_t fcb_median_hist_offset(void) { return median_hist_offset(); }
+
+FCB_API int fcb_median_shard_init(int n, void* ws, size_t ws_bytes, const int* gate,
+                                  fcb_stream_t stream) {
+    return median_shard_init(n, ws, ws_bytes, gate, CS(stream));
+}
+
+FCB_API int fcb_median_shard_pass(const double* X, int n, int d, int pass, long long tile_lo,
+                                  long long tile_hi, void* ws, const int* gate,
+                                  fcb_stream_t stream) {
+    return median_shard_pass(X, n, d, pass, tile_lo, tile_hi, ws, gate, CS(stream));
+}
+
+FCB_API int fcb_median_shard_select(int n, int pass, void* ws, const int* gate,
+                                    fcb_stream_t stream) {
+    return median_shard_select(n, pass, ws, gate, CS(stream));
+}
+
+FCB_API int fcb_median_shard_finish(int n, double log_np1, double* hstat, void* ws,
+                                    const int* gate, fcb_stream_t stream) {
+    return median_shard_finish(n, log_np1, hstat, ws, gate, CS(stream));
 }
 
 }  // extern "C"

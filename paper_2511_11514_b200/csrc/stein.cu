@@ -15,6 +15,8 @@
 // * stein_flow: g_i = (1/n)[sum_j k_ij w_j + (2/h) x'_i sum_j k_ij],
 //   w_j = s_j - (2/h) x'_j, k_ij = exp(-|x_i-x_j|^2/h), fused in registers
 //   over column chunks with a fixed-order merge (no float atomics).
+#include <cstddef>
+
 #include "fcb_internal.cuh"
 
 #include <algorithm>
@@ -88,6 +90,40 @@ __global__ void __launch_bounds__(256) gmm_eval_kernel(const double* __restrict_
         }
         if (logdens) logdens[i] = M + log(S);
     }
+}
+
+// SamplePoints.sample (reference.py:140-146) on a device-resident cloud: the
+// indices are drawn on the host (numpy PCG64, bit-identical to the
+// reference) and the rows are gathered here, one thread per output element
+// so consecutive threads write consecutive doubles.  An out-of-range index
+// stores its position in *status (first one wins) and the row is left zero.
+__global__ void gather_rows_kernel(const double* __restrict__ src, int m, int d,
+                                   const int* __restrict__ idx, int n, double* __restrict__ out,
+                                   int* status) {
+    const size_t total = (size_t)n * d;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+         e += (size_t)gridDim.x * blockDim.x) {
+        const size_t i = e / d, q = e % d;
+        const int j = __ldg(idx + i);
+        if (j < 0 || j >= m) {
+            out[e] = 0.0;
+            if (q == 0 && status) atomicCAS(status, -1, (int)i);
+            continue;
+        }
+        out[e] = __ldg(src + (size_t)j * d + q);
+    }
+}
+
+int gather_rows(const double* src, int m, int d, const int* idx, int n, double* out, int* status,
+                cudaStream_t st) {
+    if (n < 1) return FCB_OK;
+    if (m < 1 || d < 1) return fail(FCB_EINPUT, "gather: empty source");
+    if (status) FCB_CUDA(cudaMemsetAsync(status, 0xff, sizeof(int), st));
+    const long total = (long)n * d;
+    const int blocks = (int)std::max<long>(1, std::min<long>(8L * sm_count(), (total + 255) / 256));
+    gather_rows_kernel<<<blocks, 256, 0, st>>>(src, m, d, idx, n, out, status);
+    FCB_LAUNCHED("gather_rows_kernel");
+    return FCB_OK;
 }
 
 int gmm_eval(const double* X, int n, int d, int k, const double* prm, double* score,
@@ -197,10 +233,14 @@ __device__ __forceinline__ unsigned long long sqdist_key(const double* a, const 
     return (unsigned long long)__double_as_longlong(acc);
 }
 
+// Tiles [t_lo, t_hi) of the upper triangle of 64 x 64 pair tiles.  fold: the
+// last CTA selects the digit (single GPU); 0 leaves the histogram for an
+// all_reduce across ranks and fcb_median_select (M-sharded median).
 template <int D>
 __global__ void __launch_bounds__(MED_BLOCK) median_hist_kernel(const double* __restrict__ X, int n,
                                                                 MedState* st, int pass,
-                                                                const int* gate) {
+                                                                const int* gate, long long t_lo,
+                                                                long long t_hi, int fold) {
     __shared__ unsigned hist[2][MED_BINS];
     __shared__ double pj[MED_TILE * D];
     if (gate && *((volatile const int*)gate) != 0) return;
@@ -211,9 +251,8 @@ __global__ void __launch_bounds__(MED_BLOCK) median_hist_kernel(const double* __
     const bool same = pre0 == pre1;
     for (int b = threadIdx.x; b < 2 * MED_BINS; b += MED_BLOCK) (&hist[0][0])[b] = 0u;
     const int nb = (n + MED_TILE - 1) / MED_TILE;
-    const long long ntiles = (long long)nb * (nb + 1) / 2;
     __syncthreads();
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (long long t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x) {
         // map t -> (bi, bj) with bi <= bj (row-major upper triangle)
         int bi = (int)((2.0 * nb + 1.0 - sqrt((2.0 * nb + 1.0) * (2.0 * nb + 1.0) - 8.0 * t)) / 2.0);
         bi = max(0, min(bi, nb - 1));
@@ -251,6 +290,7 @@ __global__ void __launch_bounds__(MED_BLOCK) median_hist_kernel(const double* __
         if (hist[0][b]) atomicAdd(&st->hist[0][b], (unsigned long long)hist[0][b]);
         if (!same && hist[1][b]) atomicAdd(&st->hist[1][b], (unsigned long long)hist[1][b]);
     }
+    if (!fold) return;
     // the last CTA of the pass selects the digit (no separate launch)
     __shared__ int s_last;
     __threadfence();
@@ -327,14 +367,69 @@ int median_bandwidth(const double* X, int n, int d, double log_np1, double* hsta
     const int grid = (int)std::min<long long>(ntiles, 4LL * sm_count());
     for (int pass = 0; pass < MED_PASSES; ++pass) {
         switch (d) {
-            case 1: median_hist_kernel<1><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate); break;
-            case 2: median_hist_kernel<2><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate); break;
-            case 3: median_hist_kernel<3><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate); break;
+            case 1: median_hist_kernel<1><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate, 0, ntiles, 1); break;
+            case 2: median_hist_kernel<2><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate, 0, ntiles, 1); break;
+            case 3: median_hist_kernel<3><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate, 0, ntiles, 1); break;
             default: return fail(FCB_ENOTSUP, "dimension must be 1, 2 or 3");
         }
         FCB_LAUNCHED("median_hist_kernel");
     }
     median_finish_kernel<<<1, 32, 0, st>>>(ms, n, log_np1, hstat, gate);
+    FCB_LAUNCHED("median_finish_kernel");
+    return FCB_OK;
+}
+
+// ---- the M-sharded median (distributed.py): per radix pass, every rank
+// histograms its share of the pair tiles, the caller all-reduces the
+// histogram (MedState.hist, 2 x MED_BINS unsigned long long at byte offset
+// median_hist_offset()), then every rank selects the same digit.
+__global__ void median_select_kernel(MedState* st, int n, int pass, const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    median_select_block(st, n, pass);
+}
+
+long long median_tiles(int n) {
+    const long long nb = (n + MED_TILE - 1) / MED_TILE;
+    return nb * (nb + 1) / 2;
+}
+
+size_t median_hist_offset() { return offsetof(MedState, hist); }
+
+int median_shard_init(int n, void* ws, size_t ws_bytes, const int* gate, cudaStream_t st) {
+    if (n < 2) return fail(FCB_EINPUT, "sharded median needs n >= 2");
+    if (ws_bytes < median_ws_bytes(n)) return fail(FCB_EWORKSPACE, "median workspace too small");
+    const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
+    median_init_kernel<<<1, 256, 0, st>>>(static_cast<MedState*>(ws), (N - 1ull) / 2ull, N / 2ull,
+                                          gate);
+    FCB_LAUNCHED("median_init_kernel");
+    return FCB_OK;
+}
+
+int median_shard_pass(const double* X, int n, int d, int pass, long long t_lo, long long t_hi,
+                      void* ws, const int* gate, cudaStream_t st) {
+    if (pass < 0 || pass >= MED_PASSES) return fail(FCB_EINPUT, "median pass out of range");
+    MedState* ms = static_cast<MedState*>(ws);
+    if (t_hi <= t_lo) return FCB_OK;
+    const int grid = (int)std::min<long long>(t_hi - t_lo, 4LL * sm_count());
+    switch (d) {
+        case 1: median_hist_kernel<1><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate, t_lo, t_hi, 0); break;
+        case 2: median_hist_kernel<2><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate, t_lo, t_hi, 0); break;
+        case 3: median_hist_kernel<3><<<grid, MED_BLOCK, 0, st>>>(X, n, ms, pass, gate, t_lo, t_hi, 0); break;
+        default: return fail(FCB_ENOTSUP, "dimension must be 1, 2 or 3");
+    }
+    FCB_LAUNCHED("median_hist_kernel");
+    return FCB_OK;
+}
+
+int median_shard_select(int n, int pass, void* ws, const int* gate, cudaStream_t st) {
+    median_select_kernel<<<1, MED_BLOCK, 0, st>>>(static_cast<MedState*>(ws), n, pass, gate);
+    FCB_LAUNCHED("median_select_kernel");
+    return FCB_OK;
+}
+
+int median_shard_finish(int n, double log_np1, double* hstat, void* ws, const int* gate,
+                        cudaStream_t st) {
+    median_finish_kernel<<<1, 32, 0, st>>>(static_cast<MedState*>(ws), n, log_np1, hstat, gate);
     FCB_LAUNCHED("median_finish_kernel");
     return FCB_OK;
 }

@@ -181,6 +181,26 @@ class DeviceOps:
         self._call("fcb_median_bandwidth", _dev.ptr(X), n, d, math.log(n + 1.0), _dev.ptr(hstat),
                    _dev.ptr(gate), _dev.ptr(ws), ws.numel(), _dev.stream())
 
+    def median_sharded(self, X, hstat, gate, coll):
+        """median_bandwidth (stein.py:66-76) over this rank's pair tiles, the radix
+        histograms all-reduced per pass (fcb_median_shard_*)."""
+        n, d = X.shape
+        if n < 2:
+            return self.median_bandwidth(X, hstat, gate)
+        ws = self.workspace(self.lib.fcb_median_workspace_bytes(n), "shard_med")
+        lo, hi = shard_bounds(int(self.lib.fcb_median_tiles(n)), coll.rank, coll.world)
+        off = int(self.lib.fcb_median_hist_offset())
+        hist = ws[off:off + 2 * 2048 * 8].view(torch.int64)
+        s = _dev.stream()
+        self._call("fcb_median_shard_init", n, _dev.ptr(ws), ws.numel(), _dev.ptr(gate), s)
+        for p in range(6):
+            self._call("fcb_median_shard_pass", _dev.ptr(X), n, d, p, lo, hi, _dev.ptr(ws),
+                       _dev.ptr(gate), s)
+            coll.all_reduce_sum(hist)
+            self._call("fcb_median_shard_select", n, p, _dev.ptr(ws), _dev.ptr(gate), s)
+        self._call("fcb_median_shard_finish", n, math.log(n + 1.0), _dev.ptr(hstat),
+                   _dev.ptr(ws), _dev.ptr(gate), s)
+
     def gmm_score(self, X, k, params, out, gate):
         n, d = X.shape
         self._call("fcb_gmm_eval", _dev.ptr(X), n, d, k, _dev.ptr(params), _dev.ptr(out), None,
@@ -379,7 +399,8 @@ class ShardedStein:
     """stein_flow (stein.py:79-122) with the sources split across ranks.
 
     The bandwidth is fixed (SteinConfig.bandwidth > 0) or the exact median,
-    which every rank computes in full (replicated, identical).
+    whose pair tiles are split across the ranks with the radix histograms
+    all-reduced per pass (identical on every rank).
     """
 
     def __init__(self, n: int, d: int, q, bandwidth, group=None, ops=None,
@@ -406,7 +427,7 @@ class ShardedStein:
                   conv_tol: float = 0.0):
         ops = self.ops
         if self.bandwidth == "median":
-            ops.median_bandwidth(X, self.hstat, plan_state)
+            ops.median_sharded(X, self.hstat, plan_state, self.coll)
         ops.gmm_score(X, self.k, self.params, self.scores, plan_state)
         lo, hi = self.cols
         if hi > lo:

@@ -236,7 +236,11 @@ def plan_detailed(
         targets = None
     weights = workspace_weights(model.project_matrix, model.control_dim, cfg.q_weight, cfg.r_weight)
     want_metric = cfg.metric_interval > 0
-    q_metric = metric_targets(q, cfg, T) if want_metric else None
+    # metric draws from a point cloud are a device gather of host-drawn indices
+    # from the targets already on the device (below); mixtures draw on the host
+    metric_gather = (want_metric and isinstance(q, SamplePoints) and cfg.method == "sinkhorn"
+                     and group is None)
+    q_metric = metric_targets(q, cfg, T) if want_metric and not metric_gather else None
 
     U0 = initial_controls(cfg, model, T)
     clamp = cfg.control_clamp
@@ -319,9 +323,13 @@ def plan_detailed(
     upd_ws = _dev.Workspace.get(lib.fcb_plan_update_workspace_bytes(n_s, m_c, T), "plan_upd")
     roll_ws = _dev.Workspace.get(lib.fcb_rollout_workspace_bytes(n_s, T), "plan_roll")
     if want_metric:
-        Ym = np.atleast_2d(np.asarray(q_metric, dtype=np.float64))
-        Mm = Ym.shape[0]
-        Ymd = _dev.f64(Ym, dev)
+        if metric_gather:
+            Mm = cfg.metric_samples if cfg.metric_samples is not None else T
+            Ymd = q.sample_device(Mm, [cfg.seed, STREAM_METRIC], points=Yd)
+        else:
+            Ym = np.atleast_2d(np.asarray(q_metric, dtype=np.float64))
+            Mm = Ym.shape[0]
+            Ymd = _dev.f64(Ym, dev)
         mprec = _precision.pick(cfg.sinkhorn.precision, max(T, Mm) ** 2, cfg.sinkhorn.tol)
         met_ws = _dev.Workspace.get(
             lib.fcb_sinkhorn_divergence_workspace_bytes(mprec, T, Mm, d), "plan_metric"

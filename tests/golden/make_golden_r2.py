@@ -16,6 +16,8 @@ Two sources, both pinned to the reference:
   batch  -- the reference plans three BASELINE config-5 problems
             (single_integrator_2d, Sinkhorn, T=1000, M=4096, problem b: seed b,
             targets q.sample(4096, [b, 2])).  -> batch_cfg5_cases.npz
+  tspio  -- the reference's tours (tsp.py:120-147) on config-5-like point sets
+            and edge cases, and files its io.py wrote.  -> tsp_cases.npz, io/
   large  -- shapes the reference cannot hold (it materialises C, C^T and
             C_xx): the oracle (oracle/flowcover_oracle.py, a streaming
             restatement checked bit-for-bit against the reference by
@@ -176,12 +178,50 @@ def gen_large(which: str = ""):
     save(name, **out)
 
 
+def gen_tsp_io():
+    """Reference tours (tsp.py:120-147) for config-5-like point sets and edge
+    cases, and files written by the reference's io.py."""
+    sys.path.insert(0, REF)
+    import flowcover as fc
+    from flowcover import io as rio
+    from flowcover.tsp import build_tour
+
+    out = {}
+    q2, q3 = fc.benchmark_mixture(2), fc.benchmark_mixture(3)
+    cases = [("t0", q2.sample(1000, [0, 2]), 0, None), ("t1", q2.sample(1000, [1, 2]), 1, None),
+             ("t3d", q3.sample(300, [5, 2]), 5, None), ("tbud", q2.sample(400, [7, 2]), 7, 5),
+             ("t2", np.array([[0.0, 0.0], [1.0, 1.0]]), 3, None),
+             ("tdup", np.array([[0.5, 0.5]] * 4 + [[0.1, 0.2]] * 3), 2, None)]
+    for tag, pts, seed, budget in cases:
+        t0 = time.perf_counter()
+        tour = build_tour(pts, seed, budget)
+        print(f"  tour {tag}: {time.perf_counter() - t0:.1f}s length {tour.length:.6f}", flush=True)
+        out.update({f"{tag}_pts": pts, f"{tag}_order": tour.order,
+                    f"{tag}_meta": np.array([seed, -1 if budget is None else budget, tour.length])})
+    save("tsp_cases.npz", **out)
+    io_dir = os.path.join(HERE, "io")
+    os.makedirs(io_dir, exist_ok=True)
+    m = fc.differential_drive()
+    U = 0.1 * np.random.default_rng(3).standard_normal((25, 2))
+    S = fc.rollout(m, fc.default_start(m), U, 0.05)
+    rio.write_trajectory(os.path.join(io_dir, "traj_diff_drive.csv"),
+                         fc.Trajectory(S=S, U=U, dt=0.05), m)
+    rio.write_points(os.path.join(io_dir, "points_named.csv"), q3.sample(17, [1, 9]),
+                     names=("x", "y", "z"))
+    rio.write_points(os.path.join(io_dir, "points_plain.csv"), q2.sample(9, [2, 9]))
+    rio.write_metrics(os.path.join(io_dir, "metrics.json"),
+                      {"coverage": 0.1234567890123, "iterations": 20, "method": "sinkhorn",
+                       "phases": {"flow": 1.5, "lqr": 0.25}})
+    print("  wrote io/*", flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="plans,batch,large")
+    ap.add_argument("--only", default="plans,batch,large,tspio")
     ap.add_argument("--large", default="", help="subset of L2,L3,S3,cfg3")
     args = ap.parse_args()
-    jobs = dict(plans=gen_plans, batch=gen_batch, large=lambda: gen_large(args.large))
+    jobs = dict(plans=gen_plans, batch=gen_batch, large=lambda: gen_large(args.large),
+                tspio=gen_tsp_io)
     for name, fn in jobs.items():
         if name not in args.only.split(","):
             continue

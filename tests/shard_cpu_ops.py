@@ -194,6 +194,55 @@ class CpuOps:
         clamped = h <= 1e-12
         hstat.copy_(torch.tensor([max(h, 1e-12), med, float(clamped), 0.0], dtype=torch.float64))
 
+    def median_sharded(self, X, hstat, gate, coll):
+        """The radix selection of csrc/stein.cu over this rank's 64 x 64 pair tiles
+        (upper triangle, i < j, each pair counted twice, the n diagonal zeros
+        added in the first bucket), histograms all-reduced per pass."""
+        if gate is not None and int(gate[0]) != 0:
+            return
+        Xn = X.numpy()
+        n = Xn.shape[0]
+        nb = (n + 63) // 64
+        tiles = [(bi, bj) for bi in range(nb) for bj in range(bi, nb)]
+        lo, hi = (len(tiles) * coll.rank) // coll.world, (len(tiles) * (coll.rank + 1)) // coll.world
+        keys = []
+        for bi, bj in tiles[lo:hi]:
+            I = np.arange(bi * 64, min(n, bi * 64 + 64))
+            J = np.arange(bj * 64, min(n, bj * 64 + 64))
+            d2 = O.sqdist(Xn[I], Xn[J])
+            keep = J[None, :] > I[:, None]
+            keys.append(d2[keep])
+        keys = np.concatenate(keys).view(np.uint64) if keys else np.zeros(0, np.uint64)
+        N = n * n
+        prefix, rank = [0, 0], [(N - 1) // 2, N // 2]
+        for shift, bits in zip((52, 41, 30, 19, 8, 0), (11, 11, 11, 11, 11, 8)):
+            hshift = shift + bits
+            same = prefix[0] == prefix[1]
+            hist = np.zeros((2, 2048), dtype=np.int64)
+            hi_bits = keys >> np.uint64(hshift) if hshift < 64 else np.zeros_like(keys)
+            dig = ((keys >> np.uint64(shift)) & np.uint64((1 << bits) - 1)).astype(np.int64)
+            for t in (0,) if same else (0, 1):
+                sel = hi_bits == np.uint64(prefix[t])
+                hist[t] += 2 * np.bincount(dig[sel], minlength=2048)
+            h = torch.from_numpy(hist)
+            coll.all_reduce_sum(h)
+            hist = h.numpy()
+            for t in (0, 1):
+                hh = hist[0 if same else t].copy()
+                if prefix[t] == 0:
+                    hh[0] += n
+                csum = np.cumsum(hh)
+                b = int(np.searchsorted(csum, rank[t], side="right"))
+                rank[t] -= int(csum[b - 1]) if b > 0 else 0
+                prefix[t] = (prefix[t] << bits) | b
+        vlo = np.array([prefix[0]], dtype=np.uint64).view(np.float64)[0]
+        vhi = np.array([prefix[1]], dtype=np.uint64).view(np.float64)[0]
+        med = math.sqrt(vlo) if N % 2 else (math.sqrt(vlo) + math.sqrt(vhi)) / 2.0
+        h = med * med / math.log(n + 1.0)
+        clamped = h <= 1e-12
+        hstat.copy_(torch.tensor([1e-12 if clamped else h, med, float(clamped), 0.0],
+                                 dtype=torch.float64))
+
     def gmm_score(self, X, k, params, out, gate):
         if gate is not None and int(gate[0]) != 0:
             return

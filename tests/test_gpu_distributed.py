@@ -171,3 +171,30 @@ def test_plan_batch_single_rank():
     for s, res in enumerate(out):
         one = fc.plan(*probs[s])
         assert np.array_equal(res.trajectory.S, one.trajectory.S)
+
+
+@pytest.mark.parametrize("n,d", [(2, 2), (701, 2), (1500, 3)])
+def test_sharded_median_tiles_R3_equal_exact_median(n, d):
+    """fcb_median_shard_*: three tile ranges histogrammed into one state (what
+    the all_reduce sums on a multi-GPU run) select the exact median."""
+    import math
+
+    from paper_2511_11514_b200 import _dev
+
+    X = O.benchmark_mixture(d).sample(n, [43, d])
+    dev = D.DeviceOps()
+    lib = dev.lib
+    Xd = dev.tensor(X)
+    ws = dev.workspace(lib.fcb_median_workspace_bytes(n), "t_med")
+    ntiles = int(lib.fcb_median_tiles(n))
+    hstat = dev.zeros((4,))
+    s = _dev.stream()
+    dev._call("fcb_median_shard_init", n, _dev.ptr(ws), ws.numel(), None, s)
+    for p in range(6):
+        for r in range(3):
+            lo, hi = D.shard_bounds(ntiles, r, 3)
+            dev._call("fcb_median_shard_pass", _dev.ptr(Xd), n, d, p, lo, hi, _dev.ptr(ws), None, s)
+        dev._call("fcb_median_shard_select", n, p, _dev.ptr(ws), None, s)
+    dev._call("fcb_median_shard_finish", n, math.log(n + 1.0), _dev.ptr(hstat), _dev.ptr(ws),
+              None, s)
+    assert float(hstat[0]) == O.median_bandwidth(X) == fc.median_bandwidth(X)

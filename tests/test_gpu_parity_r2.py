@@ -199,3 +199,26 @@ def test_config5_batched_vs_reference():
         assert rel_inf(res.trajectory.U, g[f"b{b}_U"]) <= 0.01
         assert rel_inf(res.flow_norms, g[f"b{b}_flow_norms"]) <= 1e-3
         assert rel_inf(res.lqr_costs, g[f"b{b}_lqr_costs"]) <= 0.01
+
+
+# ---- device sample gather (SamplePoints.sample, reference.py:140-146) --------------
+@pytest.mark.parametrize("m,n,d", [(1, 5, 2), (1000, 4097, 1), (200_003, 100_000, 3)])
+def test_sample_device_gather_is_bit_identical(m, n, d):
+    rng = np.random.default_rng(m)
+    sp = fc.SamplePoints(rng.random((m, d)))
+    dev = sp.sample_device(n, [7, 3]).cpu().numpy()
+    assert np.array_equal(dev, sp.sample(n, [7, 3]))
+
+
+def test_plan_metric_draws_gathered_on_device_match_host_draws():
+    """metric_interval > 0 with a point-cloud target: the draws are a device
+    gather; the metric history equals a run whose draws come from the host."""
+    q = fc.benchmark_mixture(2)
+    tg = fc.SamplePoints(q.sample(3000, [0, STREAM_REFERENCE]))
+    cfg = fc.PlanConfig(method="sinkhorn", eta=30.0, max_iterations=6, convergence_tol=0.0,
+                        metric_interval=2, metric_samples=500)
+    disc = fc.Discretization(0.05, 400, np.array([0.1, 0.1]))
+    res = fc.plan(fc.single_integrator_2d(), tg, disc, cfg)
+    draws = tg.sample(500, [0, STREAM_METRIC])
+    assert res.final_metric == pytest.approx(
+        fc.coverage_metric(res.trajectory.S, fc.single_integrator_2d(), draws), rel=1e-12)
