@@ -170,3 +170,62 @@ def test_rollout_lqr_update_guards(name, T):
                                _dev.ptr(a), v.ptr, z.ptr, K.ptr, dff.ptr, scal.ptr, st.ptr,
                                w.ptr, _dev.stream()), "lqr")
     check(v, z, K, dff, scal, st, w)
+
+
+def test_gather_and_tour_guards():
+    L = lib()
+    rng = np.random.default_rng(5)
+    src = _dev.f64(rng.random((1001, 3)))
+    idx = torch.from_numpy(rng.integers(0, 1001, size=777).astype(np.int32)).cuda()
+    out, status = Guarded((777, 3)), Guarded((1,), torch.int32)
+    _lib.check(L.fcb_gather_rows(_dev.ptr(src), 1001, 3, _dev.ptr(idx), 777, out.ptr, status.ptr,
+                                 _dev.stream()), "gather")
+    check(out, status)
+    assert int(status.view[0]) == -1
+    pts = _dev.f64(rng.random((3, 333, 2)))
+    starts = torch.tensor([0, 5, 332], dtype=torch.int32, device="cuda")
+    order, moves = Guarded((3, 333), torch.int32), Guarded((3,), torch.int32)
+    _lib.check(L.fcb_tsp_tours(_dev.ptr(pts), 3, 333, 2, _dev.ptr(starts), 3330, order.ptr,
+                               moves.ptr, _dev.stream()), "tsp")
+    check(order, moves)
+    for b in range(3):
+        assert sorted(order.view[b].tolist()) == list(range(333))
+
+
+def test_sharded_step_guards():
+    from paper_2511_11514_b200 import distributed as D
+
+    rng = np.random.default_rng(6)
+    n, m, d, R = 517, 1301, 3, 3
+    X, Y = _dev.f64(rng.random((n, d))), _dev.f64(rng.random((m, d)))
+    L = lib()
+    ysum = Guarded((d + 2,))
+    _lib.check(L.fcb_point_sums(_dev.ptr(Y), m, d, ysum.ptr, _dev.stream()), "sums")
+    scal_x, scal_s, f, p = Guarded((16,)), Guarded((16,)), Guarded((n,)), Guarded((n,))
+    ctl, eslot = Guarded((8,), torch.int32), Guarded((2,), torch.int64)
+    _lib.check(L.fcb_shard_init(0, _dev.ptr(X), n, d, ysum.ptr, 0.0, None, None, None, scal_x.ptr,
+                                scal_s.ptr, f.ptr, p.ptr, ctl.ptr, eslot.ptr, None,
+                                _dev.stream()), "init")
+    gath = _dev.f64(np.concatenate([np.c_[rng.normal(size=(n, 1)) - 3, rng.random((n, d))]
+                                    for _ in range(R)]))
+    fnext, rs, mass, ybar, stat = (Guarded((n,)), Guarded((n,)), Guarded((n,)), Guarded((n, d)),
+                                   Guarded((4,)))
+    _lib.check(L.fcb_shard_cross_merge(n, d, R, _dev.ptr(gath), scal_x.ptr, 1e-6, 3, f.ptr,
+                                       fnext.ptr, rs.ptr, mass.ptr, ybar.ptr, ctl.ptr, eslot.ptr,
+                                       stat.ptr, _dev.stream()), "merge")
+    check(ysum, scal_x, scal_s, f, p, ctl, eslot, fnext, rs, mass, ybar, stat)
+    chunk = (n + R - 1) // R
+    lo, hi = D.shard_bounds(n, 1, R)
+    Lb = _dev.f64(np.c_[rng.normal(size=(hi - lo, 1)), rng.random((hi - lo, d))])
+    send = Guarded((chunk, d + 4))
+    _lib.check(L.fcb_shard_self_rows(n, d, lo, hi - lo, _dev.ptr(Lb), scal_s.ptr, p.ptr, send.ptr,
+                                     ctl.ptr, _dev.stream()), "self rows")
+    check(send, p)
+    parts = _dev.f64(rng.random((R, n, d + 1)))
+    hstat = _dev.f64([0.02, np.nan, 0.0, 0.0])
+    flow, fstat = Guarded((n, d)), Guarded((8,))
+    w = ws(L.fcb_stein_combine_workspace_bytes(n))
+    _lib.check(L.fcb_stein_combine(_dev.ptr(X), n, d, R, _dev.ptr(parts), _dev.ptr(hstat),
+                                   flow.ptr, fstat.ptr, None, 0, None, 0.0, w.ptr, w.view.numel(),
+                                   _dev.stream()), "combine")
+    check(flow, fstat, w)
