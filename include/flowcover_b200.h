@@ -397,6 +397,10 @@ FCB_API int fcb_peak_probe(int which, int iters, double* out, fcb_stream_t strea
  * count and resets the log.  Production builds return 0. */
 FCB_API int fcb_debug_timeline(unsigned long long* host_out, int cap);
 
+/* Work items of the chunked solver that fell back from the fp32 fast path to
+ * the careful loop since the last call (synchronises the device; resets). */
+FCB_API long long fcb_debug_careful_items(void);
+
 #ifdef __cplusplus
 }
 #endif

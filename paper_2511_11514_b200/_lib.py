@@ -134,6 +134,7 @@ SIGNATURES: dict[str, tuple] = {
     "fcb_tsp_tours": (_I, [_P, _I, _I, _I, _P, _I, _P, _P, _P]),
     "fcb_peak_probe": (_I, [_I, _I, _P, _P]),
     "fcb_debug_timeline": (_I, [_P, _I]),
+    "fcb_debug_careful_items": (ctypes.c_longlong, []),
 }
 
 _lock = threading.Lock()

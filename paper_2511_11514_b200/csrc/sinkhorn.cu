@@ -447,11 +447,15 @@ __device__ __forceinline__ bool sweep_item_f32(const Vec4<float>* __restrict__ r
 #pragma unroll
         for (int q = 0; q < D; ++q) acc[r][q] = make_float2(0.f, 0.f);
     }
-    if (!est.trust) {
-        // no usable potential estimate (first sweep of a cold solve): shift
-        // each row by its max over FCB_SAMPLE columns spread over this item's
-        // chunk -- the partial sum is then >= 1; only a chunk whose best
-        // column beats the sample's by > ~2^100 falls back to the careful loop
+    {
+        // shift each row by its max over FCB_SAMPLE columns spread over this
+        // item's chunk: the sampled column contributes 2^0, so the partial sum
+        // is >= 1 and cannot underflow, and only a chunk whose best column
+        // beats the sample's by > ~2^100 overflows (careful loop).  The
+        // potential-based estimate is exact only near the fixed point; after a
+        // large planner step (config 4 moves the trajectory by hundreds of
+        // units per iteration) a warm estimate sends ~15 % of the items to the
+        // careful loop, the sample almost none.  Deterministic (fixed columns).
         constexpr int NS = FCB_SAMPLE;
         __syncthreads();
         if (tid < NS) {
@@ -554,6 +558,10 @@ __device__ __forceinline__ bool sweep_item_f32(const Vec4<float>* __restrict__ r
     return true;
 }
 
+// Items that took the careful scalar loop (fp32 fast path refused), for
+// fcb_debug_careful_items (diagnostics; one atomic per refused item).
+__device__ unsigned g_careful_items;
+
 // All items of a sweep.  Item blockIdx.x is static (no atomic before the
 // first item); the rest are handed out dynamically, so CTAs that run faster
 // (an SM shared with a slower neighbour, earlier start) take more items.  The
@@ -584,6 +592,7 @@ __device__ __forceinline__ void run_sweep(const Sweep& sw, const Vec4<Real>* row
                                                 reinterpret_cast<float*>(s_tile), est, pm, ps, pa,
                                                 ldp, ch);
         }
+        if (!done && EXP && threadIdx.x == 0) atomicAdd(&g_careful_items, 1u);
         if (!done)
             sweep_item<Real, D, RPT, EXP, BARY>(rows, sw.rows, rb * OT_BLOCK * RPT,
                                                 cols.for_block(rb), c0, c1, s_tile, s, est, pm, ps,
@@ -1746,4 +1755,11 @@ extern "C" FCB_API int fcb_debug_timeline(unsigned long long* host_out, int cap)
     (void)cap;
     return 0;
 #endif
+}
+
+extern "C" FCB_API long long fcb_debug_careful_items(void) {
+    unsigned v = 0, zero = 0;
+    if (cudaMemcpyFromSymbol(&v, fcb::g_careful_items, sizeof(unsigned)) != cudaSuccess) return -1;
+    cudaMemcpyToSymbol(fcb::g_careful_items, &zero, sizeof(unsigned));
+    return (long long)v;
 }
