@@ -94,7 +94,7 @@ struct OtArgs {
     Real* pa2;
     Sweep A, B;
     GridBarrier* bar;
-    unsigned long long* errslot;  // 3 slots + [3]: tag of the g left in gbuf (ASYM)
+    unsigned long long* errslot;  // 3 slots
     double* f_out;
     double* g_out;
     double* rs_out;
@@ -229,7 +229,6 @@ struct ShiftEst {
     double logw;        // log a (rows X) or log b (rows Y)
     double inv_w;       // 1 / omega
     double unit;        // exponent units per natural unit
-    int trust = 0;      // 1: close enough for the fp32 fast path (not a cold first sweep)
     __device__ __forceinline__ double at(int i) const {
         if (!pot) return 0.0;
         const double v = unit * (logw - __ldcg(pot + i) * inv_w);
@@ -785,7 +784,7 @@ __device__ __forceinline__ void sweep_only_pass(const OtArgs<Real>& p, const OtS
     const double* c = sc.c;
     const double csc = EXP ? 2.0 * sc.sd : 1.0;
     const double unit = Units<Real>::unit;
-    const ShiftEst est{p.row_est, p.row_logw, 1.0 / sc.w, unit, p.row_est != nullptr};
+    const ShiftEst est{p.row_est, p.row_logw, 1.0 / sc.w, unit};
     run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colY}, s, est, p.pm, p.ps,
                                        p.pa, &p.bar->work, 0u, s_tile);
     grid_sync(p.bar);
@@ -801,16 +800,12 @@ __device__ __forceinline__ void sweep_only_pass(const OtArgs<Real>& p, const OtS
     });
 }
 
-__device__ __forceinline__ unsigned long long gbuf_tag(int m) {
-    return 0x5EEDF10C00000000ull ^ (unsigned long long)(unsigned)m;
-}
-
 // The Sinkhorn iterations of an ASYM or SYM solve (after pack_phase and a
 // grid barrier) up to convergence or max_iters, then the outputs.  wbase:
 // work-counter base, carried across solves that share the barrier.
 template <typename Real, int D, int RPT, bool BARY>
 __device__ __forceinline__ void solve_loop(const OtArgs<Real>& p, const OtScal& sc, unsigned& wbase,
-                                           double* red, Vec4<Real>* s_tile, bool warm) {
+                                           double* red, Vec4<Real>* s_tile) {
     constexpr bool EXP = (sizeof(Real) == 4);
     const double w = sc.w;
     const double sd = sc.sd;
@@ -834,18 +829,12 @@ __device__ __forceinline__ void solve_loop(const OtArgs<Real>& p, const OtScal& 
         double* pmB = asym ? p.pm2 : p.pm;
         Real* psB = asym ? p.ps2 : p.ps;
         Real* paB = asym ? p.pa2 : p.pa;
-        // the first sweep of a cold solve shifts by an estimate from f = 0:
-        // it takes the careful loop directly
-        const ShiftEst estB{fcur, p.loga, 1.0 / w, unit, (it > 1 || warm) ? 1 : 0};
+        const ShiftEst estB{fcur, p.loga, 1.0 / w, unit};
         if (asym) {
             // ---- sweep A: rows Y, columns X (potential f) --------------
-            // shift estimate: g of the previous iteration; at it == 1 of a
-            // warm-started solve, the g the previous solve on this workspace
-            // left behind (tagged with m) -- the estimate only shifts the terms
-            // (rounding), never the math; cold solves never use it, so a
-            // repeated cold call stays bit-identical
-            const bool gprev = it > 1 || (warm && __ldcg(p.errslot + 3) == gbuf_tag(p.m));
-            const ShiftEst estA{gprev ? p.gbuf : nullptr, p.logb, 1.0 / w, unit, gprev ? 1 : 0};
+            // shift estimate of the careful loop: g of the previous iteration
+            // (none at it == 1); the fp32 fast path samples its own shift
+            const ShiftEst estA{it > 1 ? p.gbuf : nullptr, p.logb, 1.0 / w, unit};
             run_sweep<Real, D, RPT, EXP, false>(p.A, p.rowY, PlainCols<Real>{p.colX}, s, estA, p.pm,
                                                 p.ps, p.pa, &p.bar->work, wbase, s_tile);
             wbase += (unsigned)p.A.items;
@@ -903,7 +892,6 @@ __device__ __forceinline__ void solve_loop(const OtArgs<Real>& p, const OtScal& 
             for (int i = gtid; i < p.n; i += gthreads) p.f_out[i] = __ldcg(fcur + i);
             if (asym && p.g_out)
                 for (int j = gtid; j < p.m; j += gthreads) p.g_out[j] = __ldcg(p.gbuf + j);
-            if (asym && gtid == 0) p.errslot[3] = gbuf_tag(p.m);
             if (gtid == 0) {
                 p.stat[0] = err;
                 p.stat[1] = (double)it;
@@ -929,7 +917,7 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) ot_solve_kernel(OtArgs<Rea
         return;
     }
     unsigned wbase = 0;
-    solve_loop<Real, D, RPT, BARY>(p, sc, wbase, red, s_tile, p.f0 != nullptr);
+    solve_loop<Real, D, RPT, BARY>(p, sc, wbase, red, s_tile);
 }
 
 // ---------------------------------------------------------------------------
@@ -1047,8 +1035,8 @@ __global__ void __launch_bounds__(OT_BLOCK, FCB_MINB) flow_kernel(FlowArgs<Real>
     grid_sync(A.bar);
 
     unsigned wbase = 0;
-    solve_loop<Real, D, RPT, true>(A, scA, wbase, red, s_tile, vf);
-    solve_loop<Real, D, RPT, true>(B, scB, wbase, red, s_tile, vp);
+    solve_loop<Real, D, RPT, true>(A, scA, wbase, red, s_tile);
+    solve_loop<Real, D, RPT, true>(B, scB, wbase, red, s_tile);
     grid_sync(A.bar);
 
     // ---- finalize: FlowError test, envelope gradient, warm state ----------
