@@ -202,3 +202,46 @@ def test_shard_bounds_partition():
     assert np.array_equal(np.concatenate(parts), Y)
     assert max(p.shape[0] for p in parts) - min(p.shape[0] for p in parts) <= 1
     assert [shard_bounds(23, r, 4) for r in range(4)] == [(0, 5), (5, 11), (11, 17), (17, 23)]
+
+
+def _uneven_worker(rank, world, port, X, Y, out_dir):
+    _init(rank, world, port)
+    from shard_cpu_ops import CpuOps
+
+    from paper_2511_11514_b200 import FlowError, SinkhornConfig
+    from paper_2511_11514_b200.distributed import ShardedSinkhornFlow, shard_rows
+
+    flow = ShardedSinkhornFlow(shard_rows(Y, rank, world),
+                               SinkhornConfig(omega=0.03, tol=1e-10, max_iters=5000),
+                               group=dist.group.WORLD, ops=CpuOps())
+    st: dict = {}
+    a = flow(X, stats=st)
+    # an iteration budget too small for the tolerance: every rank raises FlowError
+    tight = ShardedSinkhornFlow(shard_rows(Y, rank, world),
+                                SinkhornConfig(omega=0.03, tol=1e-12, max_iters=2),
+                                group=dist.group.WORLD, ops=CpuOps())
+    raised = False
+    try:
+        tight(X)
+    except FlowError:
+        raised = True
+    np.savez(os.path.join(out_dir, f"u{rank}.npz"), a=a.a, raised=np.array(raised),
+             inner=np.array([st["iters_cross"], st["iters_self"]]))
+    dist.destroy_process_group()
+
+
+def test_three_ranks_uneven_shards_and_flow_error(tmp_path):
+    """world 3: neither n = 50 nor m = 101 divides evenly (shards of 16/17 self
+    rows and 33/34 samples); the budget-starved solve raises FlowError on every
+    rank, as sinkhorn.py:370-373 does."""
+    rng = np.random.default_rng(11)
+    X, Y = rng.random((50, 2)), rng.random((101, 2))
+    mp.spawn(_uneven_worker, args=(3, _free_port(), X, Y, str(tmp_path)), nprocs=3, join=True)
+    res = [dict(np.load(tmp_path / f"u{r}.npz")) for r in range(3)]
+    for r in range(1, 3):
+        assert np.array_equal(res[0]["a"], res[r]["a"])
+    assert all(bool(r["raised"]) for r in res)
+    st: dict = {}
+    ref, _, _ = O.sinkhorn_flow(X, Y, 0.03, 5000, 1e-10, stats=st)
+    assert list(res[0]["inner"]) == [st["iters_cross"], st["iters_self"]]
+    assert np.abs(res[0]["a"] - ref).max() / np.abs(ref).max() <= 1e-9
