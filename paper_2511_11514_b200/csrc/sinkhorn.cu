@@ -48,6 +48,9 @@ namespace fcb {
 #ifndef FCB_MINB
 #define FCB_MINB 2       // min resident CTAs per SM (register budget)
 #endif
+#ifndef FCB_MERGE_SPLIT
+#define FCB_MERGE_SPLIT 8  // sweep-B row blocks from which g is merged in its own pass
+#endif
 #ifndef FCB_SAMPLE
 #define FCB_SAMPLE 32    // sampled columns per item for the cold-sweep row shift
 #endif
@@ -839,12 +842,27 @@ __device__ __forceinline__ void solve_loop(const OtArgs<Real>& p, const OtScal& 
                                                 p.ps, p.pa, &p.bar->work, wbase, s_tile);
             wbase += (unsigned)p.A.items;
             grid_sync(p.bar);
-            // ---- sweep B: rows X, columns Y with g = w (log b - LSE_A)
-            // merged from sweep A's partials while staging the tiles -----
-            const MergedCols<Real> colsB{p.colY, p.rowY, p.pm, p.ps, p.A.nchunks, p.A.rows, p.m,
-                                         w, p.logb, sd, p.gbuf, nullptr};
-            run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, colsB, s, estB, pmB, psB, paB,
-                                               &p.bar->work, wbase, s_tile);
+            // ---- sweep B: rows X, columns Y with g = w (log b - LSE_A) ----
+            if (p.B.nrb >= FCB_MERGE_SPLIT) {
+                // many row blocks: merge g once per column (one pass, one grid
+                // barrier) instead of once per row block in the tile staging
+                merge_phase<Real, D, false>(p.A, p.pm, p.ps, p.pa,
+                                            [&](int j, double L, const double*) {
+                                                const double g = w * (p.logb - L);
+                                                p.gbuf[j] = g;
+                                                p.colY[j].w = (Real)(sd * g + (double)p.rowY[j].w);
+                                            });
+                grid_sync(p.bar);
+                run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colY}, s, estB,
+                                                   pmB, psB, paB, &p.bar->work, wbase, s_tile);
+            } else {
+                // few row blocks: merged from sweep A's partials while staging
+                // the tiles (no merge pass, no extra barrier)
+                const MergedCols<Real> colsB{p.colY, p.rowY, p.pm, p.ps, p.A.nchunks, p.A.rows,
+                                             p.m, w, p.logb, sd, p.gbuf, nullptr};
+                run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, colsB, s, estB, pmB, psB, paB,
+                                                   &p.bar->work, wbase, s_tile);
+            }
         } else {
             // ---- SYM: rows X, columns X --------------------------------------
             run_sweep<Real, D, RPT, EXP, BARY>(p.B, p.rowX, PlainCols<Real>{p.colX}, s, estB, pmB,
