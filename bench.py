@@ -34,8 +34,11 @@ cpu_baseline  the oracle port of the reference (numpy float64, all host
         threads) on a bounded sample of the same workload; the full step is
         infeasible on CPU (the reference would materialise 2 TB of cost
         matrices), so the step time is extrapolated from the sample's rate.
-secondary  BASELINE configs[1] (2D double integrator, Sinkhorn, T=2000,
-        M=1e4, 200 iterations), the round-1 headline, N=1 only.
+secondary  N=1 only, device-timed like `value`: configs[1] (2D double
+        integrator, Sinkhorn, T=2000, M=1e4, 200 iterations; the round-1
+        headline), configs[0] (SVGD median h, T=500, 100 iterations:
+        planner it/s), configs[2] (diff_drive, T=1e4, M=1e5) and configs[4]
+        (512 independent problems per GPU in one batched launch).
 
 --impl reference runs the oracle port's sample as the reference arm.
 """
@@ -326,7 +329,13 @@ def run_ours(args):
     secondary = None
     if rank == 0 and world == 1:
         if not args.no_secondary:
-            secondary = config2_secondary(torch, fc, _dev, lib, peak, min(args.steps, 10), flush)
+            secondary = {
+                "configs[1]": config2_secondary(torch, fc, _dev, lib, peak, min(args.steps, 10),
+                                                flush),
+                "configs[0]": config1_secondary(torch, fc, flush),
+                "configs[2]": config3_secondary(torch, fc, _dev, peak, flush),
+                "configs[4]": config5_secondary(torch, fc, peak),
+            }
         if not args.no_cpu:
             sk0 = runs[0][0]
             cpu = cpu_baseline(sk0, pairs / args.steps)
@@ -399,6 +408,73 @@ def config2_secondary(torch, fc, _dev, lib, peak, steps, flush):
             "planner_iters_per_s": sum(r.result.iterations_used for r in runs) / t,
             "flow_phase_frac_of_mufu": pairs / t_flow / peak["ex2"],
             "flow_share_of_step": t_flow / t}
+
+
+def _timed(torch, fn, reps, flush=None):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = []
+    e0.record()
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        out.append(fn())
+    e1.record()
+    e1.synchronize()
+    return out, e0.elapsed_time(e1) * 1e-3
+
+
+def config1_secondary(torch, fc, flush):
+    """BASELINE configs[0]: 2D double integrator, SVGD with the exact median
+    bandwidth, T=500, 100 iterations (the CPU-oracle config; iterations/s)."""
+    di = fc.double_integrator_2d()
+    q = fc.benchmark_mixture(2)
+    disc = fc.Discretization(DT, 500, S0_DI)
+    cfg = fc.PlanConfig(method="stein", eta=0.1, max_iterations=100, convergence_tol=0.0,
+                        metric_interval=0, seed=0)
+    runs, t = _timed(torch, lambda: fc.plan_detailed(di, q, disc, cfg), 5, flush)
+    its = sum(r.result.iterations_used for r in runs)
+    return {"workload": "BASELINE configs[0]: 2D double integrator, SVGD (median h), T=500, "
+                        "100 iterations", "planner_iters_per_s": its / t,
+            "ms_per_plan": t / len(runs) * 1e3, "pair_evals_per_s": sum(r.pairs for r in runs) / t}
+
+
+def config3_secondary(torch, fc, _dev, peak, flush):
+    """BASELINE configs[2]: diff_drive, Sinkhorn, T=1e4, M=1e5 (3 outer iterations)."""
+    m = fc.differential_drive()
+    Y = fc.benchmark_mixture(2).sample(100_000, [0, 2])
+    Yd = _dev.f64(Y)
+    disc = fc.Discretization(DT, 10_000, fc.default_start(m))
+    cfg = fc.PlanConfig(method="sinkhorn", eta=1500.0, max_iterations=3, convergence_tol=0.0,
+                        metric_interval=0, seed=0)
+    runs, t = _timed(torch, lambda: fc.plan_detailed(m, fc.SamplePoints(Y), disc, cfg,
+                                                      resident_targets=Yd), 3, flush)
+    pairs = sum(r.pairs for r in runs)
+    t_flow = sum(r.result.phase_times.flow for r in runs)
+    return {"workload": "BASELINE configs[2]: diff_drive, Sinkhorn, T=1e4, M=1e5, 3 outer iterations",
+            "value": pairs / t, "unit": UNIT, "ms_per_plan": t / len(runs) * 1e3,
+            "flow_frac_of_mufu": pairs / t_flow / peak["ex2"]}
+
+
+def config5_secondary(torch, fc, peak, problems=512, iters=100):
+    """BASELINE configs[4] per GPU: 512 independent single-integrator problems
+    (T=1000, M=4096; problem b: seed b, targets q.sample(4096, [b, 2])) in one
+    batched launch, 100 iterations each."""
+    m = fc.single_integrator_2d()
+    q = fc.benchmark_mixture(2)
+    probs = [(m, fc.SamplePoints(q.sample(4096, [b, 2])),
+              fc.Discretization(DT, 1000, np.array([0.1, 0.1])),
+              fc.PlanConfig(method="sinkhorn", eta=150.0, max_iterations=iters,
+                            convergence_tol=0.0, metric_interval=0, seed=b))
+             for b in range(problems)]
+    runs, t = _timed(torch, lambda: fc.plan_batch_detailed(probs), 1)
+    runs = runs[0]
+    pairs = sum(r.pairs for r in runs)
+    return {"workload": f"BASELINE configs[4] per GPU: {problems} independent problems, T=1000, "
+                        f"M=4096, {iters} iterations, one batched launch",
+            "seconds": t, "problems_per_s": problems / t, "value": pairs / t, "unit": UNIT,
+            "frac_of_mufu": pairs / t / peak["ex2"]}
 
 
 # ---------------------------------------------------------------------------
