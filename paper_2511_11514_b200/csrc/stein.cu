@@ -147,6 +147,7 @@ constexpr int MED_TILE = 64;
 constexpr int MED_BLOCK = 256;
 constexpr int MED_BINS = 2048;
 constexpr int MED_PASSES = 6;
+constexpr long long MED_COOP_TILES = 16384;  // one cooperative launch up to n ~ 11.5k
 __constant__ int c_med_shift[MED_PASSES] = {52, 41, 30, 19, 8, 0};
 __constant__ int c_med_bits[MED_PASSES] = {11, 11, 11, 11, 11, 8};
 
@@ -155,6 +156,7 @@ struct MedState {
     unsigned long long rank[2];    // remaining rank inside the prefix bucket
     unsigned long long hist[2][MED_BINS];
     unsigned done;                 // CTAs finished with the current pass
+    GridBarrier bar;               // median_coop_kernel
 };
 
 // The digit selection of one radix pass, by one CTA of MED_BLOCK threads:
@@ -233,21 +235,18 @@ __device__ __forceinline__ unsigned long long sqdist_key(const double* a, const 
     return (unsigned long long)__double_as_longlong(acc);
 }
 
-// Tiles [t_lo, t_hi) of the upper triangle of 64 x 64 pair tiles.  fold: the
-// last CTA selects the digit (single GPU); 0 leaves the histogram for an
-// all_reduce across ranks and fcb_median_select (M-sharded median).
+// One radix pass over tiles [t_lo, t_hi) of the upper triangle of 64 x 64
+// pair tiles (tile t handled by CTA t % gridDim.x): shared-memory histograms
+// of the current digit among keys that match the known prefix, then one
+// global atomic per nonzero bin.
 template <int D>
-__global__ void __launch_bounds__(MED_BLOCK) median_hist_kernel(const double* __restrict__ X, int n,
-                                                                MedState* st, int pass,
-                                                                const int* gate, long long t_lo,
-                                                                long long t_hi, int fold) {
-    __shared__ unsigned hist[2][MED_BINS];
-    __shared__ double pj[MED_TILE * D];
-    if (gate && *((volatile const int*)gate) != 0) return;
+__device__ __forceinline__ void median_hist_pass(const double* __restrict__ X, int n, MedState* st,
+                                                 int pass, long long t_lo, long long t_hi,
+                                                 unsigned (*hist)[MED_BINS], double* pj) {
     const int shift = c_med_shift[pass];
     const int bits = c_med_bits[pass];
     const int hshift = shift + bits;  // bits above the current digit are known
-    const unsigned long long pre0 = st->prefix[0], pre1 = st->prefix[1];
+    const unsigned long long pre0 = __ldcg(&st->prefix[0]), pre1 = __ldcg(&st->prefix[1]);
     const bool same = pre0 == pre1;
     for (int b = threadIdx.x; b < 2 * MED_BINS; b += MED_BLOCK) (&hist[0][0])[b] = 0u;
     const int nb = (n + MED_TILE - 1) / MED_TILE;
@@ -290,6 +289,20 @@ __global__ void __launch_bounds__(MED_BLOCK) median_hist_kernel(const double* __
         if (hist[0][b]) atomicAdd(&st->hist[0][b], (unsigned long long)hist[0][b]);
         if (!same && hist[1][b]) atomicAdd(&st->hist[1][b], (unsigned long long)hist[1][b]);
     }
+}
+
+// Tiles [t_lo, t_hi) of the upper triangle of 64 x 64 pair tiles.  fold: the
+// last CTA selects the digit (single GPU); 0 leaves the histogram for an
+// all_reduce across ranks and fcb_median_select (M-sharded median).
+template <int D>
+__global__ void __launch_bounds__(MED_BLOCK) median_hist_kernel(const double* __restrict__ X, int n,
+                                                                MedState* st, int pass,
+                                                                const int* gate, long long t_lo,
+                                                                long long t_hi, int fold) {
+    __shared__ unsigned hist[2][MED_BINS];
+    __shared__ double pj[MED_TILE * D];
+    if (gate && *((volatile const int*)gate) != 0) return;
+    median_hist_pass<D>(X, n, st, pass, t_lo, t_hi, hist, pj);
     if (!fold) return;
     // the last CTA of the pass selects the digit (no separate launch)
     __shared__ int s_last;
@@ -314,12 +327,12 @@ __global__ void median_init_kernel(MedState* st, unsigned long long klo, unsigne
     }
 }
 
-__global__ void median_finish_kernel(const MedState* st, int n, double log_np1, double* hstat,
-                                     const int* gate) {
-    if (gate && *((volatile const int*)gate) != 0) return;
-    if (threadIdx.x != 0) return;
-    const double vlo = __longlong_as_double((long long)st->prefix[0]);
-    const double vhi = __longlong_as_double((long long)st->prefix[1]);
+// h = med^2 / log(n+1) from the two selected order statistics (stein.py:66-76):
+// np.median averages the middle pair when n^2 is even.
+__device__ __forceinline__ void median_finish_dev(const MedState* st, int n, double log_np1,
+                                                  double* hstat) {
+    const double vlo = __longlong_as_double((long long)__ldcg(&st->prefix[0]));
+    const double vhi = __longlong_as_double((long long)__ldcg(&st->prefix[1]));
     const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
     double med;
     if (N % 2ull == 1ull) med = sqrt(vlo);
@@ -331,6 +344,45 @@ __global__ void median_finish_kernel(const MedState* st, int n, double log_np1, 
     hstat[1] = med;
     hstat[2] = clamped ? 1.0 : 0.0;
     hstat[3] = 0.0;
+}
+
+__global__ void median_finish_kernel(const MedState* st, int n, double log_np1, double* hstat,
+                                     const int* gate) {
+    if (gate && *((volatile const int*)gate) != 0) return;
+    if (threadIdx.x != 0) return;
+    median_finish_dev(st, n, log_np1, hstat);
+}
+
+// Small and mid-size point sets (config 1: n = 500, 36 tiles): the whole
+// selection in ONE cooperative launch -- init, then per radix pass the
+// histogram over the CTAs' tiles, a grid barrier, the digit selection by
+// CTA 0, a grid barrier -- instead of eight launches (at n = 500 each pass
+// launch costs ~12 us of launch latency and tail for ~1 us of work).
+template <int D>
+__global__ void __launch_bounds__(MED_BLOCK)
+    median_coop_kernel(const double* __restrict__ X, int n, MedState* st, long long ntiles,
+                       unsigned long long klo, unsigned long long khi, double log_np1,
+                       double* hstat, const int* gate) {
+    __shared__ unsigned hist[2][MED_BINS];
+    __shared__ double pj[MED_TILE * D];
+    if (gate && *((volatile const int*)gate) != 0) return;
+    if (blockIdx.x == 0) {
+        for (int b = threadIdx.x; b < 2 * MED_BINS; b += MED_BLOCK) (&st->hist[0][0])[b] = 0ull;
+        if (threadIdx.x == 0) {
+            st->prefix[0] = st->prefix[1] = 0ull;
+            st->rank[0] = klo;
+            st->rank[1] = khi;
+            st->done = 0u;
+        }
+    }
+    grid_sync(&st->bar);
+    for (int pass = 0; pass < MED_PASSES; ++pass) {
+        median_hist_pass<D>(X, n, st, pass, 0, ntiles, hist, pj);
+        grid_sync(&st->bar);
+        if (blockIdx.x == 0) median_select_block(st, n, pass);
+        grid_sync(&st->bar);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) median_finish_dev(st, n, log_np1, hstat);
 }
 
 __global__ void fixed_bandwidth_kernel(double h, double* hstat, const int* gate) {
@@ -360,10 +412,27 @@ int median_bandwidth(const double* X, int n, int d, double log_np1, double* hsta
     }
     MedState* ms = static_cast<MedState*>(ws);
     const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
-    median_init_kernel<<<1, 256, 0, st>>>(ms, (N - 1ull) / 2ull, N / 2ull, gate);
-    FCB_LAUNCHED("median_init_kernel");
     const int nb = (n + MED_TILE - 1) / MED_TILE;
     const long long ntiles = (long long)nb * (nb + 1) / 2;
+    if (ntiles <= MED_COOP_TILES) {
+        int per_sm = 0;
+        const void* kern = d == 1 ? (const void*)median_coop_kernel<1>
+                         : d == 2 ? (const void*)median_coop_kernel<2>
+                                  : (const void*)median_coop_kernel<3>;
+        FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, MED_BLOCK, 0));
+        if (per_sm >= 1 && d >= 1 && d <= 3) {
+            int grid = (int)std::min<long long>(ntiles, (long long)per_sm * sm_count());
+            unsigned long long klo = (N - 1ull) / 2ull, khi = N / 2ull;
+            FCB_CUDA(cudaMemsetAsync(&ms->bar, 0, sizeof(GridBarrier), st));
+            void* args[] = {(void*)&X, (void*)&n, (void*)&ms, (void*)&ntiles, (void*)&klo,
+                            (void*)&khi, (void*)&log_np1, (void*)&hstat, (void*)&gate};
+            FCB_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(MED_BLOCK), args, 0, st));
+            FCB_LAUNCHED("median_coop_kernel");
+            return FCB_OK;
+        }
+    }
+    median_init_kernel<<<1, 256, 0, st>>>(ms, (N - 1ull) / 2ull, N / 2ull, gate);
+    FCB_LAUNCHED("median_init_kernel");
     const int grid = (int)std::min<long long>(ntiles, 4LL * sm_count());
     for (int pass = 0; pass < MED_PASSES; ++pass) {
         switch (d) {
