@@ -715,7 +715,7 @@ static LqrWs lqr_layout(int ns, int m, int T, void* ws) {
     LqrWs L{};
     L.geom = ric_geom(T, ric_max_blocks());
     L.agg = ar.take<double>(2 * (size_t)L.geom.nwarp * 3 * ns * ns);
-    L.bagg = ar.take<double>(2 * (size_t)L.geom.nblk * 3 * ns * ns);
+    L.bagg = ar.take<double>((2 * (size_t)L.geom.nblk + 2 * RW_K2_WARPS) * 3 * ns * ns);
     L.K = ar.take<double>((size_t)T * m * ns);
     L.Lg = ar.take<double>((size_t)T * m * ns);
     L.Acl = ar.take<double>((size_t)T * ns * ns);

@@ -185,7 +185,7 @@ __device__ void lqr_shared_init(LqrShared<N, M>& s, const double* Q, const doubl
 //       with the next CTAs' suffix) and re-walks the chunk in information form,
 //       emitting K_k, H_k^-1 G_k', Acl_k, G_k per step.
 // ---------------------------------------------------------------------------
-constexpr int RW_WARPS = 16;              // warps per CTA (K1, K3)
+constexpr int RW_WARPS = 32;              // warps per CTA (K1, K3)
 constexpr int RW_BLOCK = 32 * RW_WARPS;
 constexpr int RW_K2_WARPS = 32;
 constexpr int RW_MIN_CHUNK = 8;
@@ -199,7 +199,7 @@ struct RicArgs {
     int nwarp;    // warps with a chunk slot (nblk * RW_WARPS)
     int nblk;     // CTAs of K1 / K3
     double* agg;  // 2 * nwarp * 3N^2: warp aggregates -> in-CTA suffixes (ping-pong)
-    double* bagg; // 2 * nblk * 3N^2: CTA aggregates -> their suffix scan (ping-pong)
+    double* bagg; // (2 nblk + 2 RW_K2_WARPS) * 3N^2: CTA aggregates, their suffix scan, K2 scratch
     // per-step outputs, element-major: X[e * T + k]
     double* K;    // M*N x T
     double* Lg;   // M*N x T   H^-1 G'
@@ -479,7 +479,11 @@ __device__ void riccati_k1(const Jac& jac, const RicArgs& p) {
 }
 
 // K2 (one CTA of RW_K2_WARPS warps): inclusive suffix scan over the CTA
-// aggregates, Hillis-Steele with each warp handling several items per round.
+// aggregates (bagg slot 0) into bagg slot 1, in three phases so each warp runs
+// ~3 sqrt(nblk)-ish combines instead of log2(nblk) rounds of several:
+//   1. warp w folds its contiguous group of aggregates into local suffixes;
+//   2. Hillis-Steele suffix scan over the (<= 32) group aggregates;
+//   3. every local suffix is completed with the suffix of the next groups.
 template <int N, int M>
 __device__ void riccati_k2(const RicArgs& p) {
     constexpr int ESZ = elemr_doubles<N>();
@@ -487,24 +491,58 @@ __device__ void riccati_k2(const RicArgs& p) {
     RwWarp<N, M>* slices = reinterpret_cast<RwWarp<N, M>*>(rw_smem + sizeof(LqrShared<N, M>));
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     RwWarp<N, M>& w = slices[wl];
-    double* src = p.bagg;
-    double* dst = p.bagg + (size_t)p.nblk * ESZ;
-    for (int s = 1; s < p.nblk; s <<= 1) {
-        for (int b = wl; b < p.nblk; b += RW_K2_WARPS) {
-            if (b + s < p.nblk) {
-                warp_copy<N>(src + (size_t)b * ESZ, w.E[0], lane);
-                warp_copy<N>(src + (size_t)(b + s) * ESZ, w.E[1], lane);
+    const int nb = p.nblk;
+    const double* agg = p.bagg;
+    double* suf = p.bagg + (size_t)nb * ESZ;
+    double* gbuf = p.bagg + (size_t)2 * nb * ESZ;  // 2 x RW_K2_WARPS group slots
+    const int G = (nb + RW_K2_WARPS - 1) / RW_K2_WARPS;
+    const int ng = (nb + G - 1) / G;
+    const int lo = wl * G, hi = min(lo + G, nb);
+    // 1. local suffixes of the group
+    if (lo < hi) {
+        double* cur = w.E[0];
+        double* nxt = w.E[2];
+        warp_copy<N>(agg + (size_t)(hi - 1) * ESZ, cur, lane);
+        warp_store<N>(cur, suf + (size_t)(hi - 1) * ESZ, lane);
+        for (int k = hi - 2; k >= lo; --k) {
+            warp_copy<N>(agg + (size_t)k * ESZ, w.E[1], lane);
+            warp_combine<N, M>(w.E[1], cur, nxt, w, lane);
+            warp_store<N>(nxt, suf + (size_t)k * ESZ, lane);
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+        warp_store<N>(cur, gbuf + (size_t)wl * ESZ, lane);
+    }
+    __syncthreads();
+    // 2. suffix scan over the group aggregates
+    double* gsrc = gbuf;
+    double* gdst = gbuf + (size_t)RW_K2_WARPS * ESZ;
+    for (int s = 1; s < ng; s <<= 1) {
+        if (wl < ng) {
+            if (wl + s < ng) {
+                warp_copy<N>(gsrc + (size_t)wl * ESZ, w.E[0], lane);
+                warp_copy<N>(gsrc + (size_t)(wl + s) * ESZ, w.E[1], lane);
                 warp_combine<N, M>(w.E[0], w.E[1], w.E[2], w, lane);
-                warp_store<N>(w.E[2], dst + (size_t)b * ESZ, lane);
+                warp_store<N>(w.E[2], gdst + (size_t)wl * ESZ, lane);
             } else {
                 for (int idx = lane; idx < ESZ; idx += 32)
-                    dst[(size_t)b * ESZ + idx] = __ldcg(src + (size_t)b * ESZ + idx);
+                    gdst[(size_t)wl * ESZ + idx] = __ldcg(gsrc + (size_t)wl * ESZ + idx);
             }
         }
         __syncthreads();
-        double* t = src;
-        src = dst;
-        dst = t;
+        double* t = gsrc;
+        gsrc = gdst;
+        gdst = t;
+    }
+    // 3. complete the local suffixes with the next groups' suffix
+    if (lo < hi && wl + 1 < ng) {
+        warp_copy<N>(gsrc + (size_t)(wl + 1) * ESZ, w.E[1], lane);
+        for (int k = lo; k < hi; ++k) {
+            warp_copy<N>(suf + (size_t)k * ESZ, w.E[0], lane);
+            warp_combine<N, M>(w.E[0], w.E[1], w.E[2], w, lane);
+            warp_store<N>(w.E[2], suf + (size_t)k * ESZ, lane);
+        }
     }
 }
 
@@ -524,7 +562,7 @@ __device__ void riccati_k3(const Jac& jac, const RicArgs& p) {
     const int lo = gw * p.L, hi = min(lo + p.L, total);
     if (lo >= total) return;
     const double* wsuf = p.agg + (size_t)(hs_rounds(RW_WARPS) & 1) * p.nwarp * ESZ;
-    const double* bsuf = p.bagg + (size_t)(hs_rounds(p.nblk) & 1) * p.nblk * ESZ;
+    const double* bsuf = p.bagg + (size_t)p.nblk * ESZ;  // K2's output slot
     const bool next_warp = wl + 1 < RW_WARPS;
     const bool next_block = blockIdx.x + 1 < p.nblk;
     if (next_warp && next_block) {
