@@ -89,6 +89,33 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// 2^x for two lanes on the FMA pipe instead of the MUFU (XU) pipe, for sweeps
+// whose MUFU.EX2 rate is the bound and whose issue slots have headroom: the
+// argument is clamped to [-125, 127], split x = j + f with j = rint(x) by the
+// 1.5*2^23 rounding constant, 2^f (|f| <= 1/2) from a degree-5 relative-error
+// minimax polynomial (max rel. error 2.4e-7 in fp32 Horner, the same order as
+// ex2.approx), and j is added into the exponent field.  Below -125 the result
+// is ~2^-125 instead of ex2.approx.ftz's 0 (terms are summed with >= 1);
+// above 127 it is ~2^127 (the sweep's out-of-range test still fires).
+// 14 issue slots for two values vs 2 MUFU instructions (8 XU cycles each).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fminf(fmaxf(x.x, -125.f), 127.f);
+    x.y = fminf(fmaxf(x.y, -125.f), 127.f);
+    const float2 rnd = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+    const float2 j = __fadd2_rn(x, rnd);                     // rint(x) in the low bits
+    const float2 jf = __fadd2_rn(j, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(jf, make_float2(-1.f, -1.f), x);  // exact, |f| <= 1/2
+    float2 p = __ffma2_rn(make_float2(1.32764654699713e-3f, 1.32764654699713e-3f), f,
+                          make_float2(9.675540961325169e-3f, 9.675540961325169e-3f));
+    p = __ffma2_rn(p, f, make_float2(5.550713464617729e-2f, 5.550713464617729e-2f));
+    p = __ffma2_rn(p, f, make_float2(2.4022120237350464e-1f, 2.4022120237350464e-1f));
+    p = __ffma2_rn(p, f, make_float2(6.931469440460205e-1f, 6.931469440460205e-1f));
+    p = __ffma2_rn(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+    // bits(j) = bits(1.5 * 2^23) + j, and bits(1.5 * 2^23) << 23 == 0 (mod 2^32)
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
 template <typename T> struct Vec4;
 template <> struct alignas(16) Vec4<float> { float x, y, z, w; };
 template <> struct alignas(32) Vec4<double> { double x, y, z, w; };

@@ -51,6 +51,9 @@ namespace fcb {
 #ifndef FCB_MERGE_SPLIT
 #define FCB_MERGE_SPLIT 8  // sweep-B row blocks from which g is merged in its own pass
 #endif
+#ifndef FCB_EMU_EX2
+#define FCB_EMU_EX2 0    // 1: one column pair in four takes 2^t on the FMA pipe (ex2_poly2)
+#endif
 #ifndef FCB_SAMPLE
 #define FCB_SAMPLE 32    // sampled columns per item for the cold-sweep row shift
 #endif
@@ -522,7 +525,8 @@ __device__ __forceinline__ bool sweep_item_f32(const Vec4<float>* __restrict__ r
                     for (int q = 0; q < D; ++q)
                         t = __ffma2_rn(make_float2(x[r][q], x[r][q]),
                                        make_float2(y[q][2 * u], y[q][2 * u + 1]), t);
-                    e[u] = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+                    if (FCB_EMU_EX2 && u == 3) e[u] = ex2_poly2(t);  // FMA pipe
+                    else e[u] = make_float2(ex2_approx(t.x), ex2_approx(t.y));
                 }
                 s2[r] = __fadd2_rn(s2[r], __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3])));
                 if constexpr (BARY) {
