@@ -151,6 +151,15 @@ FCB_API size_t fcb_sinkhorn_divergence_workspace_bytes(int precision, int n, int
 FCB_API int fcb_sinkhorn_divergence(int precision, const double* X, int n, const double* Y, int m, int d,
                             double omega_fixed, int max_iters, double tol, double* out,
                             const int* gate, void* ws, size_t ws_bytes, fcb_stream_t stream);
+/* The same with the OT(Y, Y) self term cached across calls:
+ * Y must be the same point set on every call that shares yy_cache (a device
+ * double[5], zeroed = empty: {valid, omega, cost, m, hits}); the M x M self
+ * solve is skipped when omega (fixed by omega_fixed, or resolved equal) and m
+ * match the cached entry.  Results are bit-identical to the uncached call. */
+FCB_API int fcb_sinkhorn_divergence_cached(int precision, const double* X, int n, const double* Y,
+                                   int m, int d, double omega_fixed, int max_iters, double tol,
+                                   double* out, const int* gate, double* yy_cache, void* ws,
+                                   size_t ws_bytes, fcb_stream_t stream);
 
 /* ---- reference density (reference.py) ---------------------------------- */
 

@@ -73,6 +73,8 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "fcb_sinkhorn_divergence_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "fcb_sinkhorn_divergence": (_I, [_I, _P, _I, _P, _I, _I, _D, _I, _D, _P, _P, _P, _Z, _P]),
+    "fcb_sinkhorn_divergence_cached": (_I, [_I, _P, _I, _P, _I, _I, _D, _I, _D, _P, _P, _P, _P, _Z,
+                                            _P]),
     "fcb_gmm_eval": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
     "fcb_gather_rows": (_I, [_P, _I, _I, _P, _I, _P, _P, _P]),
     "fcb_median_workspace_bytes": (_Z, [_I]),

@@ -66,7 +66,8 @@ int sinkhorn_flow(int precision, const double* X, int n, const double* Y, int m,
 size_t sinkhorn_divergence_ws_bytes(int precision, int n, int m, int d);
 int sinkhorn_divergence(int precision, const double* X, int n, const double* Y, int m, int d,
                         double omega_fixed, int max_iters, double tol, double* out,
-                        const int* gate, void* ws, size_t ws_bytes, cudaStream_t st);
+                        const int* gate, void* ws, size_t ws_bytes, cudaStream_t st,
+                        double* yy_cache);
 int gather_rows(const double* src, int m, int d, const int* idx, int n, double* out, int* status,
                 cudaStream_t st);
 int gmm_eval(const double* X, int n, int d, int k, const double* prm, double* score,
@@ -244,7 +245,18 @@ int fcb_sinkhorn_divergence(int precision, const double* X, int n, const double*
     if (int rc = check_pts(n, d)) return rc;
     if (n < 1 || m < 1) return fail(FCB_EINPUT, "point sets must be non-empty");
     return sinkhorn_divergence(precision, X, n, Y, m, d, omega_fixed, max_iters, tol, out, gate, ws,
-                               ws_bytes, CS(stream));
+                               ws_bytes, CS(stream), nullptr);
+}
+
+int fcb_sinkhorn_divergence_cached(int precision, const double* X, int n, const double* Y, int m,
+                                   int d, double omega_fixed, int max_iters, double tol,
+                                   double* out, const int* gate, double* yy_cache, void* ws,
+                                   size_t ws_bytes, fcb_stream_t stream) {
+    if (int rc = check_pts(n, d)) return rc;
+    if (n < 1 || m < 1) return fail(FCB_EINPUT, "point sets must be non-empty");
+    if (!yy_cache) return fail(FCB_EINPUT, "yy_cache must be a device double[5]");
+    return sinkhorn_divergence(precision, X, n, Y, m, d, omega_fixed, max_iters, tol, out, gate, ws,
+                               ws_bytes, CS(stream), yy_cache);
 }
 
 int fcb_gather_rows(const double* src, int m, int d, const int* idx, int n, double* out,

@@ -1463,6 +1463,39 @@ __global__ void ot_plan_kernel(const double* __restrict__ X, int n, const double
     }
 }
 
+// OT(Y, Y) cache of the divergence: Y is fixed for a whole
+// plan, so when omega is too (a numeric SinkhornConfig.omega) the M x M self
+// solve is run once.  cache (caller-owned double[5], zeroed = empty):
+// {valid, omega, cost, m, hits}.  Check: the self-Y solve's gate is set on a
+// hit (or when the caller's gate already stops everything); commit: a hit
+// replaces the (skipped) solve's cost, a miss stores it.  The cost of a hit is
+// the stored double, so cached and uncached divergences are bit-identical.
+__global__ void yy_cache_check_kernel(const double* scal, const double* cache, int m,
+                                      const int* gate, int* gate_yy) {
+    if (threadIdx.x == 0) {
+        const bool stop = gate && *((volatile const int*)gate) != 0;
+        const bool hit = cache[0] == 1.0 && cache[1] == scal[SC_OMEGA] && cache[3] == (double)m;
+        *gate_yy = (stop || hit) ? 1 : 0;
+    }
+}
+
+__global__ void yy_cache_commit_kernel(const double* scal, double* cache, int m,
+                                       const int* gate, double* cost_yy) {
+    if (threadIdx.x == 0) {
+        if (gate && *((volatile const int*)gate) != 0) return;
+        const bool hit = cache[0] == 1.0 && cache[1] == scal[SC_OMEGA] && cache[3] == (double)m;
+        if (hit) {
+            *cost_yy = cache[2];
+            cache[4] += 1.0;
+        } else {
+            cache[0] = 1.0;
+            cache[1] = scal[SC_OMEGA];
+            cache[2] = *cost_yy;
+            cache[3] = (double)m;
+        }
+    }
+}
+
 __global__ void divergence_combine_kernel(const double* costs, double* out) {
     if (threadIdx.x == 0) {
         out[1] = costs[0];
@@ -1668,6 +1701,7 @@ struct DivWs {
     double* scal;
     void* omega_ws;
     double *f, *g, *rs, *stat, *costs;
+    int* gate_yy;  // self-Y solve gate of the cached variant
     void* ot_ws;
     size_t ot_bytes, total;
 };
@@ -1683,6 +1717,7 @@ static DivWs div_layout(int precision, int n, int m, int d, void* ws, size_t byt
     L.rs = ar.take<double>(nm);
     L.stat = ar.take<double>(4);
     L.costs = ar.take<double>(4);
+    L.gate_yy = ar.take<int>(4);
     L.ot_bytes = std::max(ot_ws_bytes(FCB_OT_ASYM, precision, n, m, d),
                           std::max(ot_ws_bytes(FCB_OT_SYM, precision, n, n, d),
                                    ot_ws_bytes(FCB_OT_SYM, precision, m, m, d)));
@@ -1697,7 +1732,8 @@ size_t sinkhorn_divergence_ws_bytes(int precision, int n, int m, int d) {
 
 int sinkhorn_divergence(int precision, const double* X, int n, const double* Y, int m, int d,
                         double omega_fixed, int max_iters, double tol, double* out,
-                        const int* gate, void* ws, size_t ws_bytes, cudaStream_t st) {
+                        const int* gate, void* ws, size_t ws_bytes, cudaStream_t st,
+                        double* yy_cache) {
     DivWs L = div_layout(precision, n, m, d, ws, ws_bytes);
     if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "divergence workspace too small");
     int rc = resolve_omega(FCB_OT_ASYM, X, n, Y, m, d, omega_fixed, unit_for(precision), L.scal,
@@ -1718,11 +1754,21 @@ int sinkhorn_divergence(int precision, const double* X, int n, const double* Y, 
     FCB_LAUNCHED("ot_cost_kernel");
     copy_scal_kernel<<<1, 32, 0, st>>>(L.scal, L.scal, L.scal + SC_MY, d);
     FCB_LAUNCHED("copy_scal_kernel");
+    const int* gate_yy = gate;
+    if (yy_cache) {
+        yy_cache_check_kernel<<<1, 32, 0, st>>>(L.scal, yy_cache, m, gate, L.gate_yy);
+        FCB_LAUNCHED("yy_cache_check_kernel");
+        gate_yy = L.gate_yy;
+    }
     rc = ot_solve(FCB_OT_SYM, precision, Y, m, nullptr, 0, d, L.scal, max_iters, tol, nullptr, L.f,
-                  nullptr, L.rs, L.stat, nullptr, gate, L.ot_ws, L.ot_bytes, st);
+                  nullptr, L.rs, L.stat, nullptr, gate_yy, L.ot_ws, L.ot_bytes, st);
     if (rc) return rc;
     ot_cost_kernel<<<1, 1024, 0, st>>>(FCB_OT_SYM, L.f, L.rs, m, nullptr, 0, L.costs + 2);
     FCB_LAUNCHED("ot_cost_kernel");
+    if (yy_cache) {
+        yy_cache_commit_kernel<<<1, 32, 0, st>>>(L.scal, yy_cache, m, gate, L.costs + 2);
+        FCB_LAUNCHED("yy_cache_commit_kernel");
+    }
     divergence_combine_kernel<<<1, 32, 0, st>>>(L.costs, out);
     FCB_LAUNCHED("divergence_combine_kernel");
     return FCB_OK;

@@ -334,6 +334,9 @@ def plan_detailed(
         met_ws = _dev.Workspace.get(
             lib.fcb_sinkhorn_divergence_workspace_bytes(mprec, T, Mm, d), "plan_metric"
         )
+        # OT(Y, Y) of the metric draws: solved once per omega (a numeric
+        # SinkhornConfig.omega makes every later metric skip the M x M solve)
+        yy_cache = torch.zeros(5, dtype=torch.float64, device=dev)
 
     launches0 = lib.fcb_launch_count()
     marks: list[tuple] = []
@@ -388,10 +391,10 @@ def plan_detailed(
         e1.record()
         e2 = e1
         if want_metric and it % cfg.metric_interval == 0:
-            call("fcb_sinkhorn_divergence", mprec, _dev.ptr(X), T, _dev.ptr(Ymd), Mm, d,
+            call("fcb_sinkhorn_divergence_cached", mprec, _dev.ptr(X), T, _dev.ptr(Ymd), Mm, d,
                  _omega_arg(cfg.sinkhorn.omega), cfg.sinkhorn.max_iters, cfg.sinkhorn.tol,
                  _dev.ptr(metric_vals[it // cfg.metric_interval]), state_ptr,
-                 _dev.ptr(met_ws), met_ws.numel(), stream)
+                 _dev.ptr(yy_cache), _dev.ptr(met_ws), met_ws.numel(), stream)
             e2 = torch.cuda.Event(enable_timing=True)
             e2.record()
         if sharded and cfg.method == "sinkhorn":
@@ -510,9 +513,9 @@ def plan_detailed(
                 metric_iters.append(it)
                 metric_values.append(float(vals[it // cfg.metric_interval]))
         fm = _dev.empty((4,), device=dev)
-        call("fcb_sinkhorn_divergence", mprec, _dev.ptr(X), T, _dev.ptr(Ymd), Mm, d,
+        call("fcb_sinkhorn_divergence_cached", mprec, _dev.ptr(X), T, _dev.ptr(Ymd), Mm, d,
              _omega_arg(cfg.sinkhorn.omega), cfg.sinkhorn.max_iters, cfg.sinkhorn.tol,
-             _dev.ptr(fm), None, _dev.ptr(met_ws), met_ws.numel(), stream)
+             _dev.ptr(fm), None, _dev.ptr(yy_cache), _dev.ptr(met_ws), met_ws.numel(), stream)
         final_metric = float(fm[0].item())
         if not metric_iters or metric_iters[-1] != updates:
             metric_iters.append(updates)

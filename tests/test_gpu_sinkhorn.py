@@ -258,3 +258,66 @@ def test_ragged_and_tiny_shapes():
         scale = max(np.abs(r["f"]).max(), np.abs(r["g"]).max())  # f may vanish (n = 1)
         assert np.abs(f32.f - r["f"]).max() <= FLOW_TOL * scale, (n, m)
         assert np.abs(f32.g - r["g"]).max() <= FLOW_TOL * scale, (n, m)
+
+
+# ---- OT(Y, Y) cache of the divergence ---------------------
+def _div_call(name, X, Y, omega, prec, cache=None):
+    from paper_2511_11514_b200 import _dev, _lib
+    lib = _lib.load()
+    n, d = X.shape
+    m = Y.shape[0]
+    Xd, Yd = _dev.f64(X), _dev.f64(Y)
+    out = _dev.empty((4,))
+    ws = _dev.Workspace.get(lib.fcb_sinkhorn_divergence_workspace_bytes(prec, n, m, d), "t_div")
+    args = [prec, _dev.ptr(Xd), n, _dev.ptr(Yd), m, d, omega, 1000, 1e-6, _dev.ptr(out), None]
+    if cache is not None:
+        args.append(_dev.ptr(cache))
+    _lib.call(name, *args, _dev.ptr(ws), ws.numel(), _dev.stream(), what=name)
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_divergence_yy_cache_bit_identical(prec):
+    """The cached call skips the M x M self solve when omega and m match, and
+    returns exactly the uncached values; auto omega on a moved X misses."""
+    import torch
+    from paper_2511_11514_b200 import _lib
+    rng = np.random.default_rng(5)
+    Y = rng.random((900, 2))
+    cache = torch.zeros(5, dtype=torch.float64, device="cuda")
+    p = _lib.FCB_FP64 if prec else _lib.FCB_FP32
+    for k, omega in enumerate([0.05, 0.05, 0.05]):
+        X = rng.random((300 + 50 * k, 2))
+        ref = _div_call("fcb_sinkhorn_divergence", X, Y, omega, p)
+        got = _div_call("fcb_sinkhorn_divergence_cached", X, Y, omega, p, cache)
+        assert np.array_equal(ref, got), (k, ref, got)
+        c = cache.cpu().numpy()
+        assert c[0] == 1.0 and c[1] > 0 and c[3] == 900 and c[4] == k  # hits so far
+    # auto omega: resolved from X's moments, so a different X misses
+    hits = float(cache[4])
+    X = rng.random((300, 2)) * 0.5
+    ref = _div_call("fcb_sinkhorn_divergence", X, Y, 0.0, p)
+    got = _div_call("fcb_sinkhorn_divergence_cached", X, Y, 0.0, p, cache)
+    assert np.array_equal(ref, got)
+    assert float(cache[4]) == hits
+    # a different m never hits
+    Y2 = Y[:700]
+    ref = _div_call("fcb_sinkhorn_divergence", X, Y2, 0.05, p)
+    got = _div_call("fcb_sinkhorn_divergence_cached", X, Y2, 0.05, p, cache)
+    assert np.array_equal(ref, got) and float(cache[4]) == hits and float(cache[3]) == 700
+
+
+def test_plan_metric_with_fixed_omega_uses_cache():
+    """plan() with a numeric omega and an in-loop metric: every metric value
+    equals the public sinkhorn_divergence of that iteration's trajectory."""
+    model = fc.single_integrator_2d()
+    q = fc.benchmark_mixture(2)
+    scfg = fc.SinkhornConfig(omega=0.02, precision="float64")
+    cfg = fc.PlanConfig(method="sinkhorn", eta=60.0, max_iterations=4, convergence_tol=0.0,
+                        metric_interval=2, metric_samples=400, seed=0, sinkhorn=scfg)
+    tg = fc.SamplePoints(q.sample(600, [0, 2]))
+    res = fc.plan(model, tg, fc.Discretization(0.05, 300, np.array([0.1, 0.1])), cfg)
+    draws = tg.sample(400, [0, 3])
+    final = fc.coverage_metric(res.trajectory.S, model, draws, scfg)
+    assert res.metric_iterations[-1] == 4
+    assert abs(res.metric_values[-1] - final) <= 1e-12 * max(1.0, abs(final))
