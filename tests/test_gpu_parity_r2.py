@@ -222,3 +222,49 @@ def test_plan_metric_draws_gathered_on_device_match_host_draws():
     draws = tg.sample(500, [0, STREAM_METRIC])
     assert res.final_metric == pytest.approx(
         fc.coverage_metric(res.trajectory.S, fc.single_integrator_2d(), draws), rel=1e-12)
+
+
+# ---- the fp32 fast path's refusal -> careful scalar loop -------------------
+# At a tiny omega the row shift sampled from 32 columns of a chunk sits
+# thousands of log2 units below the row's best column, the fast path's sums
+# overflow, and every such work item is redone by the careful loop
+# (sinkhorn.cu sweep_item / g_careful_items).  The result must still be the
+# reference's: the fallback is part of the product path, not a debug mode.
+def _careful_inputs(n, m, seed):
+    rng = np.random.default_rng(seed)
+    return rng.random((n, 2)), rng.random((m, 2)), rng.random(m)
+
+
+def test_fp32_sweep_fallback_to_careful_loop_matches_oracle():
+    from paper_2511_11514_b200.sinkhorn import lse_sweep
+    X, Y, pot = _careful_inputs(1024, 4096, 21)
+    omega = 5e-5
+    lib = _lib.load()
+    lib.fcb_debug_careful_items()
+    L = lse_sweep(X, Y, pot, omega, "float32")
+    refused = lib.fcb_debug_careful_items()
+    assert refused > 0, "the inputs must exercise the careful loop"
+    ref = O.lse_sweep(X, Y, pot, omega)
+    assert rel_inf(L, ref) <= 2e-6
+    # the same sweep at a benign omega stays on the fast path
+    L2 = lse_sweep(X, Y, pot, 0.05, "float32")
+    assert lib.fcb_debug_careful_items() == 0
+    assert rel_inf(L2, O.lse_sweep(X, Y, pot, 0.05)) <= 2e-6
+
+
+def test_fp32_solve_with_careful_items_matches_oracle():
+    X, Y, _ = _careful_inputs(1024, 2048, 22)
+    omega, iters = 5e-5, 4
+    lib = _lib.load()
+    lib.fcb_debug_careful_items()
+    sol = fc.entropic_ot(X, Y, fc.SinkhornConfig(max_iters=iters, tol=1e-30,
+                                                  precision="float32"), omega=omega)
+    assert lib.fcb_debug_careful_items() > 0
+    f, g, rs, err, it, conv = O.solve_asymmetric(X, Y, omega, iters, 1e-30)
+    assert sol.iters_used == it == iters
+    # omega = 5e-5 makes the potentials themselves ~1e-4 (cost scale 2): the
+    # fp32 bound is absolute, eps32-level against the cost scale, so the check
+    # is relative to max C rather than to max |f|
+    cscale = float(O.sqdist(X, Y).max())
+    assert np.abs(sol.f - f).max() <= 1e-6 * cscale
+    assert np.abs(sol.g - g).max() <= 1e-6 * cscale
