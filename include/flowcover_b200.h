@@ -410,6 +410,11 @@ FCB_API int fcb_debug_timeline(unsigned long long* host_out, int cap);
  * the careful loop since the last call (synchronises the device; resets). */
 FCB_API long long fcb_debug_careful_items(void);
 
+/* Rows of the resident flow kernel (rs_flow_kernel) whose fp32 streaming pass
+ * was refused and redone by the careful pass since the last call
+ * (synchronises the device; resets). */
+FCB_API long long fcb_debug_careful_rows_resident(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -137,6 +137,7 @@ SIGNATURES: dict[str, tuple] = {
     "fcb_peak_probe": (_I, [_I, _I, _P, _P]),
     "fcb_debug_timeline": (_I, [_P, _I]),
     "fcb_debug_careful_items": (ctypes.c_longlong, []),
+    "fcb_debug_careful_rows_resident": (ctypes.c_longlong, []),
 }
 
 _lock = threading.Lock()

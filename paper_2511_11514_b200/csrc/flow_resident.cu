@@ -89,6 +89,13 @@ int sinkhorn_flow_resident(const double* X, int n, const double* Y, int m, int d
     }
 }
 
+extern "C" FCB_API long long fcb_debug_careful_rows_resident(void) {
+    unsigned v = 0, zero = 0;
+    if (cudaMemcpyFromSymbol(&v, g_rs_careful_rows, sizeof(unsigned)) != cudaSuccess) return -1;
+    cudaMemcpyToSymbol(g_rs_careful_rows, &zero, sizeof(unsigned));
+    return (long long)v;
+}
+
 extern "C" FCB_API int fcb_debug_rs_timeline(unsigned long long* host_out, int cap) {
 #ifdef FCB_TIMELINE
     unsigned n = 0;

@@ -214,6 +214,11 @@ __device__ __forceinline__ float2 rs_ex2_poly2(float2 t) {
                        __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(y.y) << 23)));
 }
 
+// Rows whose streaming pass was refused and redone by rs_careful (diagnostics
+// for the parity tests; one atomic per refused row, off the common path).
+// static: every translation unit that instantiates the kernels has its own.
+static __device__ unsigned g_rs_careful_rows;
+
 // A row sum is trusted in [2^-64, 2^120]: below, nothing has been
 // accumulated under a too-high shift estimate; above (or inf / NaN), the
 // terms overflowed.  Positive floats order like their bit patterns, so the
@@ -400,6 +405,7 @@ __device__ __forceinline__ void rs_rows(const RsCols& cols, int cg_log, const Rs
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
             if (!rs_out_of_range(sum[r])) continue;
+            if (r < gn) atomicAdd(&g_rs_careful_rows, 1u);
             RsRowState st;
 #pragma unroll
             for (int q = 0; q < D; ++q) st.x[q] = x[r][q];

@@ -86,11 +86,17 @@ def test_resident_and_forced_chunked_fp32_flows_vs_oracle(monkeypatch, d, n, m):
     X2 = G.step_along(X, ref1)
     st_o2: dict = {}
     ref2, _, _ = O.sinkhorn_flow(X2, Y, warm=warm_o, workers=os.cpu_count() or 1, stats=st_o2)
+    lib = _lib.load()
     for resident in ("1", "0"):
         monkeypatch.setenv("FCB_RESIDENT", resident)
         warm = fc.SinkhornWarmState()
+        lib.fcb_debug_careful_rows_resident()
+        lib.fcb_debug_careful_items()
         a1, st1, kern = _flow(X, Y, warm)
         assert kern == ("rs_flow_kernel" if resident == "1" else "flow_kernel"), (resident, kern)
+        # which fallback the cold flow took (reported; the parity bar below holds either way)
+        print(f"d={d} resident={resident}: careful rows {lib.fcb_debug_careful_rows_resident()}, "
+              f"careful items {lib.fcb_debug_careful_items()}")
         assert (st1["iters_cross"], st1["iters_self"]) == (st_o["iters_cross"], st_o["iters_self"])
         assert rel_inf(a1.a, ref1) <= FLOW_TOL, (resident, rel_inf(a1.a, ref1))
         assert rel_inf(warm.f, f1) <= FLOW_TOL and rel_inf(warm.p, p1) <= FLOW_TOL
@@ -268,3 +274,27 @@ def test_fp32_solve_with_careful_items_matches_oracle():
     cscale = float(O.sqdist(X, Y).max())
     assert np.abs(sol.f - f).max() <= 1e-6 * cscale
     assert np.abs(sol.g - g).max() <= 1e-6 * cscale
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_resident_flow_careful_rows_vs_oracle(monkeypatch, d):
+    """Rows far from every target point: in the cold first sweeps their terms
+    all sit > 2^90 below the potential-based shift, the streaming sums
+    underflow and the resident kernel redoes those rows in rs_careful.  The
+    flow must still match the oracle (and the chunked kernel)."""
+    q = O.benchmark_mixture(d)
+    X, Y = q.sample(1500, [23, d]), q.sample(5000, [0, 2])
+    X[:6] = 3.0 + 0.01 * np.arange(6 * d).reshape(6, d)  # outliers at ~3-4 from the cloud
+    st_o: dict = {}
+    ref, _, _ = O.sinkhorn_flow(X, Y, workers=os.cpu_count() or 1, stats=st_o)
+    lib = _lib.load()
+    for resident in ("1", "0"):
+        monkeypatch.setenv("FCB_RESIDENT", resident)
+        lib.fcb_debug_careful_rows_resident()
+        a, st, kern = _flow(X, Y)
+        rows = lib.fcb_debug_careful_rows_resident()
+        assert kern == ("rs_flow_kernel" if resident == "1" else "flow_kernel")
+        if resident == "1":
+            assert rows > 0, "the outliers must exercise rs_careful"
+        assert (st["iters_cross"], st["iters_self"]) == (st_o["iters_cross"], st_o["iters_self"])
+        assert rel_inf(a.a, ref) <= FLOW_TOL, (resident, rel_inf(a.a, ref))
