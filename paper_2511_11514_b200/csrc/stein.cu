@@ -19,6 +19,8 @@
 
 #include "fcb_internal.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 namespace fcb {
@@ -329,10 +331,11 @@ __global__ void median_init_kernel(MedState* st, unsigned long long klo, unsigne
 
 // h = med^2 / log(n+1) from the two selected order statistics (stein.py:66-76):
 // np.median averages the middle pair when n^2 is even.
-__device__ __forceinline__ void median_finish_dev(const MedState* st, int n, double log_np1,
-                                                  double* hstat) {
-    const double vlo = __longlong_as_double((long long)__ldcg(&st->prefix[0]));
-    const double vhi = __longlong_as_double((long long)__ldcg(&st->prefix[1]));
+__device__ __forceinline__ void median_finish_vals(unsigned long long klo_bits,
+                                                   unsigned long long khi_bits, int n,
+                                                   double log_np1, double* hstat) {
+    const double vlo = __longlong_as_double((long long)klo_bits);
+    const double vhi = __longlong_as_double((long long)khi_bits);
     const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
     double med;
     if (N % 2ull == 1ull) med = sqrt(vlo);
@@ -344,6 +347,309 @@ __device__ __forceinline__ void median_finish_dev(const MedState* st, int n, dou
     hstat[1] = med;
     hstat[2] = clamped ? 1.0 : 0.0;
     hstat[3] = 0.0;
+}
+
+__device__ __forceinline__ void median_finish_dev(const MedState* st, int n, double log_np1,
+                                                  double* hstat) {
+    median_finish_vals(__ldcg(&st->prefix[0]), __ldcg(&st->prefix[1]), n, log_np1, hstat);
+}
+
+// ---------------------------------------------------------------------------
+// Small point sets (config 1: n = 500, 124750 pairs): ONE thread-block
+// cluster.  The CTAs split the upper-triangle pairs, compute each distance key
+// once into shared memory (pass 0) and re-scan their keys in the later passes;
+// per pass the histograms are merged over distributed shared memory (each CTA
+// sums a slice of the bins of every CTA into CTA 0) and CTA 0 selects the
+// digit.  Three cluster barriers per pass instead of two grid barriers through
+// global memory and no global atomics (the cooperative kernel spends ~9 us per
+// pass at n = 500 on 36 CTAs).
+// ---------------------------------------------------------------------------
+constexpr int MCL_BLOCK = 1024;
+constexpr int MCL_SLICE = 2 * MED_BINS;  // bins of both targets
+
+struct MclShared {
+    unsigned long long pre[2], rank[2];  // identical in every CTA
+    unsigned long long warp[2 * (MCL_BLOCK / 32)];
+    unsigned long long wbase[2][MCL_BLOCK / 32];
+    unsigned long long nw[2][3];
+    unsigned long long bcnt[2];  // count of the selected bin (pairs x2, zeros included)
+    unsigned ncand;              // CTA 0: candidates gathered for the final select
+};
+constexpr int MCL_CAND = 1024;  // candidate cap of the final O(m^2) rank select
+
+inline size_t mcl_smem_bytes(int n, int d, long long keys_per_cta) {
+    return align_up((size_t)n * d * sizeof(double), 16) + (size_t)keys_per_cta * 8 +
+           2 * (size_t)MCL_SLICE * sizeof(unsigned);
+}
+
+// digit selection over the merged (2 x MED_BINS) counts (both targets at
+// once; warp totals scanned by one warp), run by every CTA on its own copy of
+// the merged histogram.
+__device__ void mcl_select(const unsigned* merged, int n, int pass, MclShared& sh) {
+    constexpr int PER = MED_BINS / MCL_BLOCK;
+    constexpr int NW = MCL_BLOCK / 32;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int bits = c_med_bits[pass];
+    const int nbins = 1 << bits;
+    const unsigned long long p0 = sh.pre[0], p1 = sh.pre[1];
+    const bool same = p0 == p1;
+    unsigned long long c[2][PER], sum[2], incl[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const unsigned* h = merged + (same ? 0 : t) * MED_BINS;
+        const unsigned long long zeros = ((t ? p1 : p0) == 0ull) ? (unsigned long long)n : 0ull;
+        sum[t] = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int b = tid * PER + k;
+            c[t][k] = (b < nbins) ? (unsigned long long)h[b] + (b == 0 ? zeros : 0ull) : 0ull;
+            sum[t] += c[t][k];
+        }
+        incl[t] = sum[t];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long v = __shfl_up_sync(0xffffffffu, incl[t], o);
+            if (lane >= o) incl[t] += v;
+        }
+        if (lane == 31) sh.warp[t * NW + wid] = incl[t];
+    }
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of the warp totals, both targets
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const unsigned long long w = sh.warp[t * NW + lane];
+            unsigned long long x = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long v = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += v;
+            }
+            sh.wbase[t][lane] = x - w;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const unsigned long long excl = sh.wbase[t][wid] + incl[t] - sum[t];
+        const unsigned long long r = sh.rank[t];
+        const bool last = tid == MCL_BLOCK - 1;
+        if ((r >= excl && r < excl + sum[t]) || (last && r >= excl + sum[t])) {
+            unsigned long long rr = r - excl;
+            int b = tid * PER;
+            unsigned long long cb = 0;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                cb = c[t][k];
+                if (rr < c[t][k] || k == PER - 1) break;
+                rr -= c[t][k];
+                ++b;
+            }
+            b = min(b, nbins - 1);
+            sh.nw[t][0] = ((t ? p1 : p0) << bits) | (unsigned long long)b;
+            sh.nw[t][1] = rr;
+            sh.nw[t][2] = cb;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        sh.pre[0] = sh.nw[0][0];
+        sh.rank[0] = sh.nw[0][1];
+        sh.bcnt[0] = sh.nw[0][2];
+        sh.pre[1] = sh.nw[1][0];
+        sh.rank[1] = sh.nw[1][1];
+        sh.bcnt[1] = sh.nw[1][2];
+    }
+    __syncthreads();
+}
+
+// Final select among the gathered candidates (CTA 0): the multiset of bucket
+// t is z zeros (the diagonal, while the prefix is 0) followed by every
+// candidate twice (pairs i<j stand for (i,j) and (j,i)); the key at the
+// remaining rank is the candidate with 2 less <= r < 2 (less + eq).
+__device__ void mcl_resolve(const unsigned long long* cand, int m, int kshift, int n,
+                            MclShared& sh) {
+    __shared__ unsigned long long s_res[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const unsigned long long pre = sh.pre[t];
+        const unsigned long long z = (pre == 0ull) ? (unsigned long long)n : 0ull;
+        const unsigned long long rr = sh.rank[t];
+        if (threadIdx.x == 0 && rr < z) s_res[t] = 0ull;
+        if (rr >= z) {
+            const unsigned long long r = rr - z;
+            for (int i = threadIdx.x; i < m; i += MCL_BLOCK) {
+                const unsigned long long c = cand[i];
+                if ((c >> kshift) != pre) continue;
+                unsigned long long less = 0, eq = 0;
+                for (int j = 0; j < m; ++j) {
+                    const unsigned long long x = cand[j];
+                    if ((x >> kshift) != pre) continue;
+                    less += x < c;
+                    eq += x == c;
+                }
+                if (2ull * less <= r && r < 2ull * (less + eq)) s_res[t] = c;  // equal writers
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sh.pre[0] = s_res[0];
+        sh.pre[1] = s_res[1];
+    }
+    __syncthreads();
+}
+
+#ifdef MCL_TL
+__device__ unsigned long long g_mcl_tl[2][64];
+#define MCL_MARK(slot)                                                               \
+    do {                                                                             \
+        if (threadIdx.x == 0 && (rank == 0 || rank == NCT - 1)) {                    \
+            unsigned long long t_;                                                   \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+            g_mcl_tl[rank == 0 ? 0 : 1][slot] = t_;                                  \
+        }                                                                            \
+    } while (0)
+#else
+#define MCL_MARK(slot) \
+    do {               \
+    } while (0)
+#endif
+template <int D, int NCT>
+__global__ void __launch_bounds__(MCL_BLOCK)
+    median_cluster_kernel(const double* __restrict__ X, int n, long long keys_per_cta,
+                          unsigned long long klo, unsigned long long khi, double log_np1,
+                          double* hstat, const int* gate) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char mcl_smem[];
+    __shared__ MclShared sh;
+    if (gate && *((volatile const int*)gate) != 0) return;  // uniform over the cluster
+    const int rank = (int)cluster.block_rank();
+    const int tid = threadIdx.x;
+    double* xs = reinterpret_cast<double*>(mcl_smem);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(
+        mcl_smem + (((size_t)n * D * sizeof(double) + 15) & ~(size_t)15));
+    unsigned* hist = reinterpret_cast<unsigned*>(keys + keys_per_cta);  // 2 x MED_BINS
+    unsigned* merged = hist + MCL_SLICE;                                 // CTA 0: 2 x MED_BINS
+    MCL_MARK(0);
+    for (int k = tid; k < n * D; k += MCL_BLOCK) xs[k] = X[k];
+    if (tid == 0) {
+        sh.pre[0] = sh.pre[1] = 0ull;
+        sh.rank[0] = klo;
+        sh.rank[1] = khi;
+        sh.ncand = 0u;
+    }
+    __syncthreads();
+    // this CTA's run [p0, p1) of the row-major upper-triangle pairs (i < j)
+    const long long P = (long long)n * (n - 1) / 2;
+    const long long p0 = P * rank / NCT, p1 = P * (rank + 1) / NCT;
+    const int cnt = (int)(p1 - p0);
+    MCL_MARK(42);
+    {
+        // pairs i < j folded into an H x W rectangle: rectangle row r holds
+        // triangle row r (n-1-r pairs) followed by its partner row, so a pair
+        // index needs one division instead of a square root (the key pass is
+        // issue-bound on the cluster's 16 SMs)
+        const bool even = (n & 1) == 0;
+        const int W = even ? n - 1 : n;
+        const float invW = 1.0f / (float)W;
+        for (int k = tid; k < cnt; k += MCL_BLOCK) {
+            const int q = (int)(p0 + k);
+            int r = (int)((float)q * invW);
+            if (r * W > q) --r;
+            else if ((r + 1) * W <= q) ++r;
+            const int c = q - r * W;
+            const int len = n - 1 - r;
+            int i, j;
+            if (c < len) {
+                i = r;
+                j = r + 1 + c;
+            } else {
+                i = even ? n - 1 - r : n - 2 - r;
+                j = i + 1 + (c - len);
+            }
+            keys[k] = sqdist_key<D>(xs + (size_t)i * D, xs + (size_t)j * D);
+        }
+    }
+    for (int pass = 0; pass < MED_PASSES; ++pass) {
+        MCL_MARK(1 + 6 * pass);
+        const int shift = c_med_shift[pass];
+        const int bits = c_med_bits[pass];
+        const int hshift = shift + bits;
+        const unsigned long long pre0 = sh.pre[0], pre1 = sh.pre[1];
+        const bool same = pre0 == pre1;
+        for (int b = tid; b < MCL_SLICE; b += MCL_BLOCK) hist[b] = 0u;
+        __syncthreads();
+        for (int k = tid; k < cnt; k += MCL_BLOCK) {
+            const unsigned long long key = keys[k];
+            const unsigned long long hi = (hshift >= 64) ? 0ull : (key >> hshift);
+            const unsigned dig = (unsigned)((key >> shift) & ((1ull << bits) - 1ull));
+            if (hi == pre0) atomicAdd(&hist[dig], 2u);
+            if (!same && hi == pre1) atomicAdd(&hist[MED_BINS + dig], 2u);
+        }
+        __syncthreads();
+        MCL_MARK(2 + 6 * pass);
+        cluster.sync();  // every CTA's histogram complete
+        MCL_MARK(3 + 6 * pass);
+        {
+            // slice `rank` of the bins, summed over the cluster, written into
+            // EVERY CTA's merged histogram (the stores spread over all the
+            // receivers' shared-memory ports; one CTA reading for everyone
+            // would serialise on its port)
+            constexpr int PERB = MCL_SLICE / NCT;
+            if (tid < PERB) {
+                const int b = rank * PERB + tid;
+                unsigned v[NCT];
+#pragma unroll
+                for (int r = 0; r < NCT; ++r) v[r] = *cluster.map_shared_rank(hist + b, r);
+                unsigned acc = 0;
+#pragma unroll
+                for (int r = 0; r < NCT; ++r) acc += v[r];
+#pragma unroll
+                for (int r = 0; r < NCT; ++r) *cluster.map_shared_rank(merged + b, r) = acc;
+            }
+        }
+        MCL_MARK(4 + 6 * pass);
+        cluster.sync();  // merged histogram complete in every CTA
+        MCL_MARK(5 + 6 * pass);
+        mcl_select(merged, n, pass, sh);  // identical inputs -> identical prefixes
+        MCL_MARK(6 + 6 * pass);
+        // few keys left in the selected bucket(s): gather them into CTA 0 and
+        // select exactly there instead of running the remaining passes
+        const int kshift = shift;  // bits >= shift of the answers are known now
+        if (pass + 1 < MED_PASSES) {
+            unsigned long long m = 0;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                if (t == 1 && sh.pre[1] == sh.pre[0]) break;
+                const unsigned long long z = (sh.pre[t] == 0ull) ? (unsigned long long)n : 0ull;
+                m += (sh.bcnt[t] - min(z, sh.bcnt[t])) / 2ull;
+            }
+            if (m <= (unsigned long long)MCL_CAND) {  // uniform over the cluster
+                unsigned long long* cand0 =
+                    reinterpret_cast<unsigned long long*>(cluster.map_shared_rank(hist, 0));
+                unsigned* nc0 = cluster.map_shared_rank(&sh.ncand, 0);
+                const unsigned long long q0 = sh.pre[0], q1 = sh.pre[1];
+                for (int k = tid; k < cnt; k += MCL_BLOCK) {
+                    const unsigned long long key = keys[k];
+                    const unsigned long long hi = key >> kshift;
+                    if (hi == q0 || hi == q1) {
+                        const unsigned slot = atomicAdd(nc0, 1u);
+                        if (slot < (unsigned)MCL_CAND) cand0[slot] = key;
+                    }
+                }
+                cluster.sync();  // candidates complete in CTA 0
+                if (rank == 0)
+                    mcl_resolve(reinterpret_cast<const unsigned long long*>(hist),
+                                (int)min(sh.ncand, (unsigned)MCL_CAND), kshift, n, sh);
+                break;
+            }
+        }
+    }
+    MCL_MARK(40);
+    cluster.sync();  // no CTA exits while others may still read its shared memory
+    MCL_MARK(41);
+    if (rank == 0 && tid == 0) median_finish_vals(sh.pre[0], sh.pre[1], n, log_np1, hstat);
 }
 
 __global__ void median_finish_kernel(const MedState* st, int n, double log_np1, double* hstat,
@@ -396,6 +702,110 @@ __global__ void fixed_bandwidth_kernel(double h, double* hstat, const int* gate)
     }
 }
 
+// One cluster of 16 CTAs (8 where 16 is not schedulable) when every CTA's keys
+// fit in shared memory; FCB_ENOTSUP otherwise (the caller falls back to the
+// cooperative / multi-launch selection).
+#ifndef FCB_MED_CLUSTER
+#define FCB_MED_CLUSTER 1
+#endif
+template <int D, int NCT>
+static cudaError_t mcl_launch(const cudaLaunchConfig_t& cfg, const double* X, int n, long long per,
+                              unsigned long long klo, unsigned long long khi, double log_np1,
+                              double* hstat, const int* gate) {
+    return cudaLaunchKernelEx(&cfg, median_cluster_kernel<D, NCT>, X, n, per, klo, khi, log_np1,
+                              hstat, gate);
+}
+
+template <int NCT>
+static const void* mcl_kernel(int d) {
+    return d == 1 ? (const void*)median_cluster_kernel<1, NCT>
+         : d == 2 ? (const void*)median_cluster_kernel<2, NCT>
+                  : (const void*)median_cluster_kernel<3, NCT>;
+}
+
+static int median_cluster_launch(const double* X, int n, int d, double log_np1, double* hstat,
+                                 const int* gate, cudaStream_t st) {
+    if (!FCB_MED_CLUSTER || d < 1 || d > 3 || n < 2) return FCB_ENOTSUP;
+    const long long P = (long long)n * (n - 1) / 2;
+    static int max_smem = -1;
+    if (max_smem < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) !=
+            cudaSuccess)
+            max_smem = 0;
+    }
+    // per (d, cluster size): the dynamic shared memory already granted, and
+    // whether the cluster is schedulable at all (host calls cost ~us each and
+    // this runs once per Stein iteration)
+    static size_t granted[4][2] = {};
+    static int usable[4][2] = {};  // 0 unknown, 1 yes, -1 no
+    for (int nct : {16, 8}) {
+        const int ci = nct == 16 ? 0 : 1;
+        const long long per = (P + nct - 1) / nct;
+        const size_t smem = mcl_smem_bytes(n, d, per);
+        if (smem + sizeof(MclShared) + 1024 > (size_t)max_smem || usable[d][ci] < 0) continue;
+        const void* kern = nct == 16 ? mcl_kernel<16>(d) : mcl_kernel<8>(d);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nct);
+        cfg.blockDim = dim3(MCL_BLOCK);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = nct;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (smem > granted[d][ci]) {
+            if ((nct > 8 && cudaFuncSetAttribute(
+                                kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                                cudaSuccess) ||
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem) != cudaSuccess) {
+                cudaGetLastError();
+                usable[d][ci] = -1;
+                continue;
+            }
+            int clusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess ||
+                clusters < 1) {
+                cudaGetLastError();
+                continue;  // not at this size (larger smem); smaller sets may still fit
+            }
+            granted[d][ci] = smem;
+            usable[d][ci] = 1;
+        }
+        const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
+        const unsigned long long klo = (N - 1ull) / 2ull, khi = N / 2ull;
+        cudaError_t e;
+        if (nct == 16) {
+            e = d == 1 ? mcl_launch<1, 16>(cfg, X, n, per, klo, khi, log_np1, hstat, gate)
+              : d == 2 ? mcl_launch<2, 16>(cfg, X, n, per, klo, khi, log_np1, hstat, gate)
+                       : mcl_launch<3, 16>(cfg, X, n, per, klo, khi, log_np1, hstat, gate);
+        } else {
+            e = d == 1 ? mcl_launch<1, 8>(cfg, X, n, per, klo, khi, log_np1, hstat, gate)
+              : d == 2 ? mcl_launch<2, 8>(cfg, X, n, per, klo, khi, log_np1, hstat, gate)
+                       : mcl_launch<3, 8>(cfg, X, n, per, klo, khi, log_np1, hstat, gate);
+        }
+        FCB_CUDA(e);
+        FCB_LAUNCHED("median_cluster_kernel");
+        return FCB_OK;
+    }
+    return FCB_ENOTSUP;
+}
+
+extern "C" FCB_API int fcb_debug_mcl_timeline(unsigned long long* out) {
+#ifdef MCL_TL
+    cudaDeviceSynchronize();
+    return cudaMemcpyFromSymbol(out, g_mcl_tl, sizeof(g_mcl_tl)) == cudaSuccess ? 128 : -1;
+#else
+    (void)out;
+    return -1;
+#endif
+}
+
 size_t median_ws_bytes(int n) {
     (void)n;
     return align_up(sizeof(MedState), 256);
@@ -414,6 +824,7 @@ int median_bandwidth(const double* X, int n, int d, double log_np1, double* hsta
     const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
     const int nb = (n + MED_TILE - 1) / MED_TILE;
     const long long ntiles = (long long)nb * (nb + 1) / 2;
+    if (median_cluster_launch(X, n, d, log_np1, hstat, gate, st) == FCB_OK) return FCB_OK;
     if (ntiles <= MED_COOP_TILES) {
         int per_sm = 0;
         const void* kern = d == 1 ? (const void*)median_coop_kernel<1>

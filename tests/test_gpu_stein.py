@@ -123,3 +123,20 @@ def test_trajectory_flow_skips_start():  # test_stein.py:105-124
     dd = fc.differential_drive()
     S = fc.rollout(dd, np.zeros(3), rng.normal(scale=0.5, size=(25, 2)), 0.05)
     assert fc.stein_flow_on_trajectory(S, dd, q).a.shape == (25, 2)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_median_cluster_and_cooperative_paths_exact(d):
+    """Small sets take the one-cluster selection (keys in shared memory,
+    histograms merged over DSMEM), larger ones the cooperative kernel; both
+    select exactly numpy's median (bit-identical bandwidths)."""
+    from paper_2511_11514_b200 import _lib
+    rng = np.random.default_rng(40 + d)
+    for n, want in ((500, "median_cluster_kernel"), (801, "median_cluster_kernel"),
+                    (1500, "median_coop_kernel")):
+        for ties in (False, True):
+            X = rng.random((n, d))
+            if ties:
+                X = np.round(X * 6) / 6
+            assert fc.median_bandwidth(X) == O.median_bandwidth(X), (n, d, ties)
+            assert _lib.last_kernel() == want, (n, d, _lib.last_kernel())
