@@ -20,6 +20,7 @@
 #include "fcb_internal.cuh"
 
 #include <cooperative_groups.h>
+#include <mutex>
 
 #include <algorithm>
 
@@ -727,6 +728,9 @@ static int median_cluster_launch(const double* X, int n, int d, double log_np1, 
                                  const int* gate, cudaStream_t st) {
     if (!FCB_MED_CLUSTER || d < 1 || d > 3 || n < 2) return FCB_ENOTSUP;
     const long long P = (long long)n * (n - 1) / 2;
+    // the one-time attribute setup below is shared by all host threads
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
     static int max_smem = -1;
     if (max_smem < 0) {
         int dev = 0;
