@@ -18,6 +18,10 @@ Two sources, both pinned to the reference:
             targets q.sample(4096, [b, 2])).  -> batch_cfg5_cases.npz
   tspio  -- the reference's tours (tsp.py:120-147) on config-5-like point sets
             and edge cases, and files its io.py wrote.  -> tsp_cases.npz, io/
+  track  -- the reference's whole baseline_plan (tour + arc-length resampling +
+            iterated TV-LQR tracking, tsp.py:150-316) for single_integrator_2d,
+            diff_drive and aircraft_3d, and track_waypoints on a path with
+            repeated points.  -> track_cases.npz
   large  -- shapes the reference cannot hold (it materialises C, C^T and
             C_xx): the oracle (oracle/flowcover_oracle.py, a streaming
             restatement checked bit-for-bit against the reference by
@@ -215,13 +219,42 @@ def gen_tsp_io():
     print("  wrote io/*", flush=True)
 
 
+def gen_track():
+    """The reference's whole TSP baseline (tsp.py:276-316: targets, tour, arc-length
+    resampling, iterated TV-LQR tracking) for the three liftable models, and
+    track_waypoints on a path with repeated points (zero-length segments)."""
+    sys.path.insert(0, REF)
+    import flowcover as fc
+
+    out = {}
+    cases = [("si", fc.single_integrator_2d(), 2, 300, 0), ("dd", fc.differential_drive(), 2, 300, 1),
+             ("ac", fc.aircraft_3d(), 3, 200, 2)]
+    for tag, model, d, T, seed in cases:
+        q = fc.benchmark_mixture(d)
+        disc = fc.Discretization(0.05, T, fc.default_start(model))
+        t0 = time.perf_counter()
+        res = fc.baseline_plan(model, q, disc, fc.BaselineConfig(seed=seed))
+        print(f"  baseline {tag}: {time.perf_counter() - t0:.1f}s", flush=True)
+        out.update({f"{tag}_S": res.trajectory.S, f"{tag}_U": res.trajectory.U,
+                    f"{tag}_order": res.tour.order, f"{tag}_waypoints": res.waypoints,
+                    f"{tag}_meta": np.array([seed, T])})
+    W = np.array([[0.1, 0.1], [0.1, 0.1], [0.4, 0.2], [0.4, 0.2], [0.4, 0.2], [0.7, 0.6],
+                  [0.3, 0.8], [0.3, 0.8]])
+    S, U = fc.track_waypoints(fc.differential_drive(), W, 120, 0.05, iterations=6)
+    out.update({"rep_W": W, "rep_S": S, "rep_U": U})
+    out["rs_in"] = W
+    out["rs_out"] = fc.resample_arclength(W, 37)
+    out["rs_single"] = fc.resample_arclength(W[:2], 5)
+    save("track_cases.npz", **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="plans,batch,large,tspio")
+    ap.add_argument("--only", default="plans,batch,large,tspio,track")
     ap.add_argument("--large", default="", help="subset of L2,L3,S3,cfg3")
     args = ap.parse_args()
     jobs = dict(plans=gen_plans, batch=gen_batch, large=lambda: gen_large(args.large),
-                tspio=gen_tsp_io)
+                tspio=gen_tsp_io, track=gen_track)
     for name, fn in jobs.items():
         if name not in args.only.split(","):
             continue

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import paper_2511_11514_b200 as fc
-from fcb_testutil import GOLDEN
+from fcb_testutil import GOLDEN, load_golden
 from paper_2511_11514_b200 import io as fio
 
 IO = os.path.join(GOLDEN, "io")
@@ -73,3 +73,14 @@ def _write(tmp_path, text):
     p = tmp_path / "x.csv"
     p.write_text(text)
     return p
+
+
+def test_resample_arclength_matches_reference():
+    """Host half of the baseline's tracking stage (tsp.py:150-167), bit for bit."""
+    from paper_2511_11514_b200.tsp import resample_arclength
+    g = load_golden("track_cases.npz")
+    np.testing.assert_array_equal(resample_arclength(g["rs_in"], 37), g["rs_out"])
+    np.testing.assert_array_equal(resample_arclength(g["rs_in"][:2], 5), g["rs_single"])
+    np.testing.assert_array_equal(resample_arclength(np.ones((3, 2)), 4), np.ones((4, 2)))
+    with pytest.raises(ValueError):
+        resample_arclength(np.ones((2, 2)), 0)
