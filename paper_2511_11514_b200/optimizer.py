@@ -666,7 +666,33 @@ def plan_batch_detailed(problems: list) -> list[PlanRun]:
     costs_all = lqr_costs.cpu().numpy()
     pn_all = phase_ns.cpu().numpy().astype(np.float64) * 1e-9
     fst = fstat.cpu().numpy()
-    roll_ws = _dev.Workspace.get(lib.fcb_rollout_workspace_bytes(n_s, T), "batch_roll")
+    # final rollouts on the last controls (optimizer.py:271-277): the B
+    # single-warp rollouts are independent, so they run concurrently on side
+    # streams with one synchronisation and bulk copies for the whole batch
+    S_fin = _dev.zeros((B, T + 1, n_s), device=dev)
+    X_fin = _dev.zeros((B, T, d), device=dev)
+    fin_status = torch.full((B,), -1, dtype=torch.int32, device=dev)
+    method = rollout_method(T)
+    side = [torch.cuda.Stream(device=dev) for _ in range(min(B, 16))]
+    nws = lib.fcb_rollout_workspace_bytes(n_s, T)
+    roll_ws = [_dev.Workspace.get(nws, f"batch_roll{k}") for k in range(len(side))]
+    ready = torch.cuda.Event()
+    ready.record()  # the buffers' fills above are on the current stream
+    for sk in side:
+        sk.wait_event(ready)
+    for b in range(B):
+        if int(st_all[b, 0]) == 2:
+            continue
+        k = b % len(side)
+        call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0[b]),
+             _dev.ptr(Ubuf[int(st_all[b, 5]) & 1][b]), T, float(disc.dt), _dev.ptr(S_fin[b]), d,
+             _dev.ptr(P), _dev.ptr(X_fin[b]), _dev.ptr(fin_status[b:b + 1]), None, 0, method,
+             _dev.ptr(roll_ws[k]), side[k].cuda_stream)
+    for sk in side:
+        sk.synchronize()
+    S_fin_h = S_fin.cpu().numpy()
+    U_h = [Ubuf[0].cpu().numpy(), Ubuf[1].cpu().numpy()]
+    fin_h = fin_status.cpu().numpy()
     runs: list[PlanRun] = []
     for b in range(B):
         stop_kind, stage_code, fail_it, fail_idx, flows_used, updates = (
@@ -687,22 +713,13 @@ def plan_batch_detailed(problems: list) -> list[PlanRun]:
                                 FlowError(flow_error_message(float(fst[b, 0]), scfg.tol)))
             raise PlanError("lqr", fail_it, trajectory_of(fail_it),
                             RiccatiDivergenceError(fail_idx))
-        # final rollout on the last controls (optimizer.py:271-277)
-        U_final = Ubuf[updates & 1][b]
-        status = torch.empty(1, dtype=torch.int32, device=dev)
-        S_final = _dev.zeros((T + 1, n_s), device=dev)
-        Xb = _dev.zeros((T, d), device=dev)
-        call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0[b]),
-             _dev.ptr(U_final), T, float(disc.dt), _dev.ptr(S_final), d, _dev.ptr(P),
-             _dev.ptr(Xb), _dev.ptr(status), None, 0, rollout_method(T), _dev.ptr(roll_ws),
-             stream)
-        fstep = int(status.item())
+        fstep = int(fin_h[b])
         if fstep >= 0:
             raise PlanError("rollout", updates, trajectory_of(flows_used - 1),
                             RolloutDivergenceError(fstep))
         log = logs[b, :flows_used].copy()
         result = PlanResult(
-            trajectory=Trajectory(S=_dev.host(S_final).copy(), U=_dev.host(U_final).copy(),
+            trajectory=Trajectory(S=S_fin_h[b].copy(), U=U_h[updates & 1][b].copy(),
                                   dt=disc.dt),
             converged=stop_kind == 1,
             iterations_used=flows_used,
