@@ -189,6 +189,9 @@ constexpr int RW_WARPS = 32;              // warps per CTA (K1, K3)
 constexpr int RW_BLOCK = 32 * RW_WARPS;
 constexpr int RW_K2_WARPS = 32;
 constexpr int RW_MIN_CHUNK = 8;
+#ifndef FCB_RIC_GENERIC
+#define FCB_RIC_GENERIC 0  // 1: generic (A, C, J) combines in the K1 walk and the K3 Phi solve
+#endif
 
 struct RicArgs {
     int T;
@@ -402,6 +405,102 @@ __device__ __forceinline__ void warp_base(bool terminal, const LqrShared<N, M>& 
     __syncwarp();
 }
 
+// out = e_k (x) acc for the step-k base element e_k = (F, G Rt^-1 G', 2 Qb)
+// of the slice's F, G (the chunk walk of K1).  With C_k of rank M the 6 x 6
+// solve of the generic combine collapses (Woodbury, Rt = 2 Rb):
+//   (I + C_k J2)^-1 = I - G (2H)^-1 G' J2,   H = Rb + G' (J2/2) G   (M x M)
+//   X_A = F - G K = Acl,  K = H^-1 G' (J2/2) F;   X_C = 1/2 G H^-1 G'
+// so  A = A2 Acl,  C = 1/2 (A2 G) H^-1 (A2 G)' + C2,  J = Acl' J2 F + 2 Qb
+// -- the Riccati step itself, one M x M solve instead of an N x N one.
+template <int N, int M>
+__device__ void warp_combine_base(const double* acc, double* out, const LqrShared<N, M>& sh,
+                                  RwWarp<N, M>& w, int lane) {
+    constexpr int NN = N * N;
+    const double *A2 = acc, *C2 = acc + NN, *J2 = acc + 2 * NN;
+    double *oA = out, *oC = out + NN, *oJ = out + 2 * NN;
+    // PG = (J2/2) G, AG = A2 G (N x M, AG in Tm), JF = J2 F (N x N, in JA)
+    for (int idx = lane; idx < 2 * N * M + NN; idx += 32) {
+        if (idx < 2 * N * M) {
+            const int which = idx / (N * M), e = idx % (N * M), i = e / M, j = e % M;
+            const double* L = which ? A2 : J2;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) s += L[i * N + q] * w.G[q * M + j];
+            if (which) w.Tm[e] = s;
+            else w.PG[e] = 0.5 * s;
+        } else {
+            const int e = idx - 2 * N * M, i = e / N, j = e % N;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) s += J2[i * N + q] * w.F[q * N + j];
+            w.JA[e] = s;
+        }
+    }
+    __syncwarp();
+    // H = Rb + G' PG;  rhs = [G' JF / 2 | (A2 G)']
+    for (int idx = lane; idx < M * M + M * 2 * N; idx += 32) {
+        if (idx < M * M) {
+            const int i = idx / M, j = idx % M;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) s += w.G[q * M + i] * w.PG[q * M + j];
+            w.H[idx] = sh.Rb[i][j] + s;
+        } else {
+            const int e = idx - M * M, i = e / (2 * N), j = e % (2 * N);
+            double s;
+            if (j < N) {
+                s = 0.0;
+#pragma unroll
+                for (int q = 0; q < N; ++q) s += w.G[q * M + i] * w.JA[q * N + j];
+                s *= 0.5;
+            } else {
+                s = w.Tm[(j - N) * M + i];
+            }
+            w.rhs[e] = s;
+        }
+    }
+    __syncwarp();
+    warp_gauss_jordan<M, 2 * N>(w.H, w.rhs, lane);  // rhs <- [K | H^-1 (A2 G)']
+    // Acl = F - G K (in Mt);  C = 1/2 (A2 G) H^-1 (A2 G)' + C2
+    for (int idx = lane; idx < NN; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        double a = 0.0, c = 0.0;
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+            a += w.G[i * M + q] * w.rhs[q * 2 * N + j];
+            c += w.Tm[i * M + q] * w.rhs[q * 2 * N + N + j];
+        }
+        w.Mt[idx] = w.F[idx] - a;
+        oC[idx] = 0.5 * c + C2[idx];
+    }
+    __syncwarp();
+    // A = A2 Acl;  J = Acl' JF + 2 Qb
+    for (int idx = lane; idx < NN; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        double a = 0.0, t = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            a += A2[i * N + q] * w.Mt[q * N + j];
+            t += w.Mt[q * N + i] * w.JA[q * N + j];
+        }
+        oA[idx] = a;
+        oJ[idx] = t + 2.0 * sh.Qb[i][j];
+    }
+    __syncwarp();
+    for (int idx = lane; idx < NN; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        if (i < j) {
+            const double c = 0.5 * (oC[i * N + j] + oC[j * N + i]);
+            const double t = 0.5 * (oJ[i * N + j] + oJ[j * N + i]);
+            oC[i * N + j] = c;
+            oC[j * N + i] = c;
+            oJ[i * N + j] = t;
+            oJ[j * N + i] = t;
+        }
+    }
+    __syncwarp();
+}
+
 template <int N>
 __device__ __forceinline__ void warp_identity(double* e, int lane) {
     constexpr int NN = N * N;
@@ -448,8 +547,12 @@ __device__ void riccati_k1(const Jac& jac, const RicArgs& p) {
         warp_base<N, M>(k0 >= p.T, sh, acc, w, lane);
         for (int k = hi - 2; k >= lo; --k) {
             warp_fg<N, M>(jac, k, p.dt, w, lane);  // k < T here
+#if FCB_RIC_GENERIC
             warp_base<N, M>(false, sh, e, w, lane);
             warp_combine<N, M>(e, acc, out, w, lane);
+#else
+            warp_combine_base<N, M>(acc, out, sh, w, lane);
+#endif
             double* t = acc;
             acc = out;
             out = t;
@@ -628,6 +731,21 @@ __device__ void riccati_k3(const Jac& jac, const RicArgs& p) {
             p.K[(size_t)idx * TT + k] = w.rhs[i * 2 * N + j];
             p.Lg[(size_t)idx * TT + k] = w.rhs[i * 2 * N + N + j];
         }
+#if !FCB_RIC_GENERIC
+        // Phi = (I + C_k J2)^-1 F equals Acl = F - G K (Woodbury with Rt = 2 Rb,
+        // see warp_combine_base): no N x N solve
+        for (int idx = lane; idx < NN; idx += 32) {
+            const int i = idx / N;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < M; ++q) s += w.G[i * M + q] * w.rhs[q * 2 * N + idx % N];
+            const double acl = w.F[idx] - s;
+            p.Acl[(size_t)idx * TT + k] = acl;
+            w.W[idx] = acl;
+        }
+        for (int idx = lane; idx < N * M; idx += 32) p.Gm[(size_t)idx * TT + k] = w.G[idx];
+        __syncwarp();
+#else
         for (int idx = lane; idx < NN; idx += 32) {
             const int i = idx / N, j = idx % N;
             double s = 0.0;
@@ -654,6 +772,7 @@ __device__ void riccati_k3(const Jac& jac, const RicArgs& p) {
         for (int idx = lane; idx < N * M; idx += 32) p.Gm[(size_t)idx * TT + k] = w.G[idx];
         __syncwarp();
         warp_gauss_jordan<N, N>(w.Mt, w.W, lane);  // W <- Phi = (I + C J2)^-1 F
+#endif
         // JF = J2 F (into JA), then J_k = Phi' JF + 2 Qb, symmetrised
         for (int idx = lane; idx < NN; idx += 32) {
             const int i = idx / N, j = idx % N;
