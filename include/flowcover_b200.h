@@ -282,6 +282,25 @@ FCB_API int fcb_plan_fused(int model, int ns, int m, const double* model_params,
                    int batch, const void* upd_ws, void* ws, size_t ws_bytes,
                    fcb_stream_t stream);
 
+/* The same persistent loop with the SVGD flow (stein.py:66-122): per iteration
+ * the rollout, the mixture score of every point, the exact median bandwidth
+ * (or bandwidth_fixed > 0), the fp64 Stein flow, the LQR affine phase and the
+ * control update in one cooperative launch over every SM, for the built-in
+ * linear models with a planar workspace and no in-loop metric (T up to 64
+ * points per SM).  gmm_params: fcb_gmm_eval's layout with k components;
+ * log_np1 = log(T + 1).  flow_log rows, fstat and plan_state as
+ * fcb_stein_flow_full + fcb_plan_update.  FCB_ENOTSUP: not covered (the
+ * caller keeps the per-iteration path). */
+FCB_API size_t fcb_plan_fused_stein_workspace_bytes(int T, int d, int m);
+FCB_API int fcb_plan_fused_stein(int model, int ns, int m, const double* model_params,
+                         const double* s0, double* U0, double* U1, double* S0, double* S1,
+                         int T, double dt, int d, const double* P, double* X, double* flow,
+                         const double* Q, const double* R, double eta, const double* clamp,
+                         int k, const double* gmm_params, double bandwidth_fixed, double log_np1,
+                         double conv_tol, double* fstat, int* plan_state, double* flow_log,
+                         double* lqr_costs, unsigned long long* phase_ns, int it0, int maxit,
+                         const void* upd_ws, void* ws, size_t ws_bytes, fcb_stream_t stream);
+
 /* ---- M-sharded flows (one process per GPU; distributed.py) ---------------
  * Replaces the row-chunked thread pool of parallel.py:47-66 (used by
  * sinkhorn.py:151-167 and stein.py:110-121) with a split of the reference

@@ -106,6 +106,12 @@ SIGNATURES: dict[str, tuple] = {
         [_I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _P, _D, _P, _P, _I, _D,
          _I, _D, _D, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _Z, _P],
     ),
+    "fcb_plan_fused_stein_workspace_bytes": (_Z, [_I, _I, _I]),
+    "fcb_plan_fused_stein": (
+        _I,
+        [_I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _D, _I, _P, _P, _P, _P, _P, _D, _P, _I, _P, _D,
+         _D, _D, _P, _P, _P, _P, _P, _I, _I, _P, _P, _Z, _P],
+    ),
     "fcb_point_sums": (_I, [_P, _I, _I, _P, _P]),
     "fcb_lse_sweep_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "fcb_lse_sweep": (_I, [_I, _P, _I, _P, _I, _I, _P, _P, _P, _D, _D, _D, _P, _P, _P, _P, _Z,

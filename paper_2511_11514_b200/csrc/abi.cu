@@ -102,6 +102,14 @@ int plan_update(int model, int ns, int m, const double* prm, const double* S, co
                 cudaStream_t st);
 
 size_t plan_fused_ws_bytes(int batch, int T, int M, int d, int mc);
+size_t plan_stein_ws_bytes(int T, int d, int mc);
+int plan_stein(int model, int ns, int m, const double* prm, const double* s0, double* U0,
+               double* U1, double* S0, double* S1, int T, double dt, int d, const double* P,
+               double* X, double* flow, const double* Q, const double* R, double eta,
+               const double* clamp, int k, const double* gmm, double bw_fixed, double log_np1,
+               double conv_tol, double* fstat, int* plan_state, double* flow_log,
+               double* lqr_costs, unsigned long long* phase_ns, int it0, int maxit,
+               const void* upd_ws, void* ws, size_t ws_bytes, cudaStream_t st);
 int plan_fused(int model, int ns, int m, const double* prm, const double* s0, double* U0,
                double* U1, double* S0, double* S1, int T, double dt, int d, const double* P,
                double* X, double* flow, const double* Q, const double* R, double eta,
@@ -329,6 +337,24 @@ int fcb_lqr_solve(int ns, int m, int T, double dt, const double* A, const double
                   fcb_stream_t stream) {
     if (!(dt > 0.0)) return fail(FCB_EINPUT, "dt must be positive");
     return lqr_solve(ns, m, T, dt, A, B, Q, R, a, v, z, K, dff, scal, status, ws, CS(stream));
+}
+
+size_t fcb_plan_fused_stein_workspace_bytes(int T, int d, int m) {
+    return plan_stein_ws_bytes(T, d, m);
+}
+
+int fcb_plan_fused_stein(int model, int ns, int m, const double* model_params, const double* s0,
+                         double* U0, double* U1, double* S0, double* S1, int T, double dt, int d,
+                         const double* P, double* X, double* flow, const double* Q,
+                         const double* R, double eta, const double* clamp, int k,
+                         const double* gmm_params, double bandwidth_fixed, double log_np1,
+                         double conv_tol, double* fstat, int* plan_state, double* flow_log,
+                         double* lqr_costs, unsigned long long* phase_ns, int it0, int maxit,
+                         const void* upd_ws, void* ws, size_t ws_bytes, fcb_stream_t stream) {
+    return plan_stein(model, ns, m, model_params, s0, U0, U1, S0, S1, T, dt, d, P, X, flow, Q, R,
+                      eta, clamp, k, gmm_params, bandwidth_fixed, log_np1, conv_tol, fstat,
+                      plan_state, flow_log, lqr_costs, phase_ns, it0, maxit, upd_ws, ws, ws_bytes,
+                      CS(stream));
 }
 
 size_t fcb_plan_fused_workspace_bytes(int batch, int T, int M, int d, int m) {

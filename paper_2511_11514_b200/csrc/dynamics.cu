@@ -879,6 +879,7 @@ int plan_update(int model, int ns, int m, const double* prm, const double* S, co
 // ---------------------------------------------------------------------------
 }  // namespace fcb
 #include "plan_fused.cuh"
+#include "plan_stein.cuh"
 namespace fcb {
 
 struct PfWs {
@@ -1043,6 +1044,176 @@ int plan_fused(int model, int ns, int m, const double* prm, const double* s0, do
                 prm, s0, U0, U1, S0, S1, T, dt, d, P, X, flow, Q, R, eta, clamp, Y, M, omega_fixed,
                 max_iters, tol, conv_tol, warm_f, warm_p, warm_valid, fstat, plan_state, flow_log,
                 lqr_costs, phase_ns, it0, maxit, batch, upd_ws, ws, ws_bytes, st);
+        default:
+            return fail(FCB_ENOTSUP, "the fused planner supports the built-in linear models");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the fused SVGD planner loop (plan_stein.cuh)
+// ---------------------------------------------------------------------------
+struct SfpWs {
+    GridBarrier* bar;
+    unsigned* done;
+    double* agg;
+    double* part;
+    int* ipart;
+    double* dff;
+    double* scores;
+    unsigned* hist;
+    unsigned long long* cand;
+    unsigned* ccount;
+    double* npart;
+    size_t total;
+};
+
+static SfpWs sfp_layout(int T, int d, int mc, void* ws, size_t bytes) {
+    Arena ar(ws, bytes);
+    SfpWs L{};
+    L.bar = ar.take<GridBarrier>(1);
+    L.done = ar.take<unsigned>(32);
+    L.agg = ar.take<double>((size_t)2 * PF_CARRY * (6 * 6 + 6));
+    L.part = ar.take<double>(PF_CARRY);
+    L.ipart = ar.take<int>(PF_CARRY);
+    L.dff = ar.take<double>((size_t)T * mc);
+    L.scores = ar.take<double>((size_t)T * d);
+    L.hist = ar.take<unsigned>((size_t)3 * 2 * SVP_BINS);
+    L.cand = ar.take<unsigned long long>(SVP_CAND);
+    L.ccount = ar.take<unsigned>(2);
+    L.npart = ar.take<double>(PF_CARRY);
+    L.total = ar.off + 256;
+    return L;
+}
+
+size_t plan_stein_ws_bytes(int T, int d, int mc) { return sfp_layout(T, d, mc, nullptr, 0).total; }
+
+template <class Mdl, int D>
+static int sfp_launch(const SvFusedArgs<Mdl::N, Mdl::M>& a, int grid, size_t smem,
+                      cudaStream_t st) {
+    auto kern = sv_plan_kernel<D, Mdl>;
+    cudaFuncAttributes fa{};
+    FCB_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));
+    if (fa.sharedSizeBytes + smem > (size_t)rs_smem_limit())
+        return fail(FCB_ENOTSUP, "fused Stein planner shared memory");
+    static size_t granted = 0;
+    if (granted < smem) {
+        FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        granted = smem;
+    }
+    int per_sm = 0;
+    FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RS_BLOCK, smem));
+    if (per_sm < 1) return fail(FCB_ENOTSUP, "fused Stein planner not co-resident");
+    SvFusedArgs<Mdl::N, Mdl::M> ac = a;
+    void* args[] = {&ac};
+    FCB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(RS_BLOCK), args, smem,
+                                         st));
+    FCB_LAUNCHED("sv_plan_kernel");
+    return FCB_OK;
+}
+
+template <class Mdl>
+static int plan_stein_t(const double* prm, const double* s0, double* U0, double* U1, double* S0,
+                        double* S1, int T, double dt, int d, const double* P, double* X,
+                        double* flow, const double* Q, const double* R, double eta,
+                        const double* clamp, int k, const double* gmm, double bw_fixed,
+                        double log_np1, double conv_tol, double* fstat, int* plan_state,
+                        double* flow_log, double* lqr_costs, unsigned long long* phase_ns,
+                        int it0, int maxit, const void* upd_ws, void* ws, size_t ws_bytes,
+                        cudaStream_t st) {
+    constexpr int N = Mdl::N, MC = Mdl::M;
+    if constexpr (!Mdl::LINEAR || N > 4) {
+        return fail(FCB_ENOTSUP, "the fused planner needs a linear model with at most 4 states");
+    } else {
+        const int G = sm_count();
+        if (G > PF_CARRY) return fail(FCB_ENOTSUP, "too many SMs for the fused planner");
+        if (d != 2) return fail(FCB_ENOTSUP, "the fused planner covers planar workspaces");
+        if ((T + G - 1) / G > 64 || T < 2)
+            return fail(FCB_ENOTSUP, "fused Stein planner: 2 <= T <= 64 x SMs");
+        // dynamic smem: scan scratch | this CTA's Riccati arrays | the column set
+        const size_t cmax = (size_t)(T + G - 1) / G;
+        const int const_off = (int)align_up(pf_smem_bytes<N>(), 16);
+        const size_t cbytes = cmax * (N * N + 3 * MC * N) * sizeof(double);
+        const int sv_off = (int)align_up(const_off + cbytes, 16);
+        const size_t smem = sv_off + (size_t)2 * T * d * sizeof(double);
+        SfpWs L = sfp_layout(T, d, MC, ws, ws_bytes);
+        if (L.total > ws_bytes) return fail(FCB_EWORKSPACE, "fused Stein workspace too small");
+        LqrWs W = lqr_layout(N, MC, T, const_cast<void*>(upd_ws));
+        FCB_CUDA(cudaMemsetAsync(L.hist, 0, (size_t)3 * 2 * SVP_BINS * sizeof(unsigned), st));
+        FCB_CUDA(cudaMemsetAsync(L.ccount, 0, 2 * sizeof(unsigned), st));
+        SvFusedArgs<N, MC> a{};
+        PlanFusedArgs<N, MC>& pf = a.pf;
+        pf.T = T;
+        pf.d = d;
+        pf.it0 = it0;
+        pf.maxit = maxit;
+        pf.dt = dt;
+        pf.eta = eta;
+        pf.s0 = s0;
+        pf.prm = prm;
+        pf.P = P;
+        pf.Q = Q;
+        pf.R = R;
+        pf.clamp = clamp;
+        pf.K = W.K;
+        pf.Lg = W.Lg;
+        pf.Acl = W.Acl;
+        pf.Gm = W.Gm;
+        pf.dff = L.dff;
+        pf.U0 = U0;
+        pf.U1 = U1;
+        pf.S0 = S0;
+        pf.S1 = S1;
+        pf.lqr_costs = lqr_costs;
+        pf.phase_ns = phase_ns;
+        pf.const_off = const_off;
+        pf.agg = L.agg;
+        pf.part = L.part;
+        pf.ipart = L.ipart;
+        a.X = X;
+        a.flow = flow;
+        a.scores = L.scores;
+        a.gmm = gmm;
+        a.k = k;
+        a.bw_fixed = bw_fixed;
+        a.log_np1 = log_np1;
+        a.conv_tol = conv_tol;
+        a.fstat = fstat;
+        a.plan_state = plan_state;
+        a.flow_log = flow_log;
+        a.hist = L.hist;
+        a.cand = L.cand;
+        a.ccount = L.ccount;
+        a.npart = L.npart;
+        a.bar = L.bar;
+        a.done = L.done;
+        a.launch_id = next_launch_epoch();
+        a.sv_off = sv_off;
+        return sfp_launch<Mdl, 2>(a, G, smem, st);
+    }
+}
+
+int plan_stein(int model, int ns, int m, const double* prm, const double* s0, double* U0,
+               double* U1, double* S0, double* S1, int T, double dt, int d, const double* P,
+               double* X, double* flow, const double* Q, const double* R, double eta,
+               const double* clamp, int k, const double* gmm, double bw_fixed, double log_np1,
+               double conv_tol, double* fstat, int* plan_state, double* flow_log,
+               double* lqr_costs, unsigned long long* phase_ns, int it0, int maxit,
+               const void* upd_ws, void* ws, size_t ws_bytes, cudaStream_t st) {
+    int rc = check_dims(model, ns, m);
+    if (rc) return rc;
+    if (it0 >= maxit) return FCB_OK;
+    if (k < 1) return fail(FCB_EINPUT, "mixture needs at least one component");
+    switch (model) {
+        case FCB_MODEL_SINGLE_INTEGRATOR_2D:
+            return plan_stein_t<Model<FCB_MODEL_SINGLE_INTEGRATOR_2D>>(
+                prm, s0, U0, U1, S0, S1, T, dt, d, P, X, flow, Q, R, eta, clamp, k, gmm, bw_fixed,
+                log_np1, conv_tol, fstat, plan_state, flow_log, lqr_costs, phase_ns, it0, maxit,
+                upd_ws, ws, ws_bytes, st);
+        case FCB_MODEL_DOUBLE_INTEGRATOR_2D:
+            return plan_stein_t<Model<FCB_MODEL_DOUBLE_INTEGRATOR_2D>>(
+                prm, s0, U0, U1, S0, S1, T, dt, d, P, X, flow, Q, R, eta, clamp, k, gmm, bw_fixed,
+                log_np1, conv_tol, fstat, plan_state, flow_log, lqr_costs, phase_ns, it0, maxit,
+                upd_ws, ws, ws_bytes, st);
         default:
             return fail(FCB_ENOTSUP, "the fused planner supports the built-in linear models");
     }

@@ -18,6 +18,7 @@
 #include <cstddef>
 
 #include "fcb_internal.cuh"
+#include "stein_dev.cuh"
 
 #include <cooperative_groups.h>
 #include <mutex>
@@ -25,8 +26,6 @@
 #include <algorithm>
 
 namespace fcb {
-
-constexpr double BANDWIDTH_FLOOR = 1e-12;  // stein.py:34
 
 // ---------------------------------------------------------------------------
 // Gaussian mixture score / log density
@@ -38,61 +37,9 @@ __global__ void __launch_bounds__(256) gmm_eval_kernel(const double* __restrict_
                                                        double* __restrict__ logdens,
                                                        const int* gate) {
     if (gate && *((volatile const int*)gate) != 0) return;
-    const double* logw = prm;
-    const double* lognorm = prm + k;
-    const double* mu = prm + 2 * k;
-    const double* chol = prm + 2 * k + (size_t)k * D;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        double x[D];
-#pragma unroll
-        for (int q = 0; q < D; ++q) x[q] = X[(size_t)i * D + q];
-        double M = -INFINITY, S = 0.0, acc[D];
-#pragma unroll
-        for (int q = 0; q < D; ++q) acc[q] = 0.0;
-        for (int c = 0; c < k; ++c) {
-            const double* L = chol + (size_t)c * D * D;
-            double diff[D], y[D], pull[D];
-#pragma unroll
-            for (int q = 0; q < D; ++q) diff[q] = x[q] - mu[(size_t)c * D + q];
-            // forward substitution L y = diff
-#pragma unroll
-            for (int r = 0; r < D; ++r) {
-                double v = diff[r];
-#pragma unroll
-                for (int q = 0; q < r; ++q) v -= L[r * D + q] * y[q];
-                y[r] = v / L[r * D + r];
-            }
-            // back substitution L^T pull = y
-#pragma unroll
-            for (int r = D - 1; r >= 0; --r) {
-                double v = y[r];
-#pragma unroll
-                for (int q = r + 1; q < D; ++q) v -= L[q * D + r] * pull[q];
-                pull[r] = v / L[r * D + r];
-            }
-            double quad = 0.0;
-#pragma unroll
-            for (int q = 0; q < D; ++q) quad += diff[q] * pull[q];
-            const double sc = -0.5 * quad - lognorm[c] + logw[c];
-            if (sc > M) {
-                const double r = (S > 0.0) ? exp(M - sc) : 0.0;
-                S = S * r + 1.0;
-#pragma unroll
-                for (int q = 0; q < D; ++q) acc[q] = acc[q] * r + pull[q];
-                M = sc;
-            } else {
-                const double r = exp(sc - M);
-                S += r;
-#pragma unroll
-                for (int q = 0; q < D; ++q) acc[q] += r * pull[q];
-            }
-        }
-        if (score) {
-#pragma unroll
-            for (int q = 0; q < D; ++q) score[(size_t)i * D + q] = -acc[q] / S;
-        }
-        if (logdens) logdens[i] = M + log(S);
-    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        gmm_point<D>(X + (size_t)i * D, k, prm, score ? score + (size_t)i * D : nullptr,
+                     logdens ? logdens + i : nullptr);
 }
 
 // SamplePoints.sample (reference.py:140-146) on a device-resident cloud: the
@@ -225,18 +172,6 @@ __device__ void median_select_block(MedState* st, int n, int pass) {
     for (int b = tid; b < 2 * MED_BINS; b += MED_BLOCK) (&st->hist[0][0])[b] = 0ull;
 }
 
-template <int D>
-__device__ __forceinline__ unsigned long long sqdist_key(const double* a, const double* b) {
-    // (a0-b0)^2 + (a1-b1)^2 [+ (a2-b2)^2], left to right, no contraction
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < D; ++q) {
-        const double df = __dsub_rn(a[q], b[q]);
-        const double sq = __dmul_rn(df, df);
-        acc = (q == 0) ? sq : __dadd_rn(acc, sq);
-    }
-    return (unsigned long long)__double_as_longlong(acc);
-}
 
 // One radix pass over tiles [t_lo, t_hi) of the upper triangle of 64 x 64
 // pair tiles (tile t handled by CTA t % gridDim.x): shared-memory histograms
@@ -330,26 +265,7 @@ __global__ void median_init_kernel(MedState* st, unsigned long long klo, unsigne
     }
 }
 
-// h = med^2 / log(n+1) from the two selected order statistics (stein.py:66-76):
-// np.median averages the middle pair when n^2 is even.
-__device__ __forceinline__ void median_finish_vals(unsigned long long klo_bits,
-                                                   unsigned long long khi_bits, int n,
-                                                   double log_np1, double* hstat) {
-    const double vlo = __longlong_as_double((long long)klo_bits);
-    const double vhi = __longlong_as_double((long long)khi_bits);
-    const unsigned long long N = (unsigned long long)n * (unsigned long long)n;
-    double med;
-    if (N % 2ull == 1ull) med = sqrt(vlo);
-    else med = __ddiv_rn(__dadd_rn(sqrt(vlo), sqrt(vhi)), 2.0);
-    double h = __ddiv_rn(__dmul_rn(med, med), log_np1);
-    const bool clamped = h <= BANDWIDTH_FLOOR;
-    if (clamped) h = BANDWIDTH_FLOOR;
-    hstat[0] = h;
-    hstat[1] = med;
-    hstat[2] = clamped ? 1.0 : 0.0;
-    hstat[3] = 0.0;
-}
-
+// the selected pair -> hstat (median_finish_vals, stein_dev.cuh)
 __device__ __forceinline__ void median_finish_dev(const MedState* st, int n, double log_np1,
                                                   double* hstat) {
     median_finish_vals(__ldcg(&st->prefix[0]), __ldcg(&st->prefix[1]), n, log_np1, hstat);

@@ -359,8 +359,16 @@ def plan_detailed(
                 and not want_metric and prec == _lib.FCB_FP32 and not sharded
                 and d == 2 and maxit > 1 and spec.model_id in (
                     _lib.FCB_MODEL_SINGLE_INTEGRATOR_2D, _lib.FCB_MODEL_DOUBLE_INTEGRATOR_2D))
+    # the same for the SVGD flow (fcb_plan_fused_stein, fp64 sweeps): iterations
+    # 1.. in one cooperative launch
+    fused_stein_ok = (os.environ.get("FCB_FUSED", "1") != "0" and cfg.method == "stein"
+                      and not want_metric and prec == _lib.FCB_FP64 and not sharded
+                      and d == 2 and maxit > 1 and spec.model_id in (
+                          _lib.FCB_MODEL_SINGLE_INTEGRATOR_2D,
+                          _lib.FCB_MODEL_DOUBLE_INTEGRATOR_2D))
     fused_ran = False
-    phase_ns = torch.zeros(3, dtype=torch.int64, device=dev) if fused_ok else None
+    phase_ns = (torch.zeros(3, dtype=torch.int64, device=dev)
+                if (fused_ok or fused_stein_ok) else None)
     for it in range(maxit):
         cur = it & 1
         if it == 1 and fused_ok:
@@ -380,6 +388,22 @@ def plan_detailed(
                 break
             if rc != _lib.FCB_ENOTSUP:
                 _lib.check(rc, "fcb_plan_fused")
+        if it == 1 and fused_stein_ok:
+            sws = _dev.Workspace.get(lib.fcb_plan_fused_stein_workspace_bytes(T, d, m_c),
+                                     "plan_fused_stein")
+            rc = lib.fcb_plan_fused_stein(
+                spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0), _dev.ptr(Ubuf[0]),
+                _dev.ptr(Ubuf[1]), _dev.ptr(Sbuf[0]), _dev.ptr(Sbuf[1]), T, float(disc.dt), d,
+                _dev.ptr(P), _dev.ptr(X), _dev.ptr(flow), _dev.ptr(Q), _dev.ptr(R),
+                float(cfg.eta), _dev.ptr(clamp_d), q.num_components, _dev.ptr(gmm), bw_fixed,
+                log_np1, float(cfg.convergence_tol), _dev.ptr(fstat), state_ptr,
+                _dev.ptr(flow_log), _dev.ptr(lqr_costs), _dev.ptr(phase_ns), 1, maxit,
+                _dev.ptr(upd_ws), _dev.ptr(sws), sws.numel(), stream)
+            if rc == _lib.FCB_OK:
+                fused_ran = True
+                break
+            if rc != _lib.FCB_ENOTSUP:
+                _lib.check(rc, "fcb_plan_fused_stein")
         if e_prev is None:
             e_prev = torch.cuda.Event(enable_timing=True)
             e_prev.record()

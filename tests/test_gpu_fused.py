@@ -125,3 +125,45 @@ def test_bench_plugin_runs_planners():
         run = planners[name](60, 1)
         assert run.trajectory.S.shape == (61, 2)
         assert run.t_flow > 0 and run.t_lqr >= 0 and run.t_rollout > 0
+
+
+# ---- the fused SVGD planner (sv_plan_kernel) --------------------------------
+@pytest.mark.parametrize("model_name,bw", [("double_integrator_2d", "median"),
+                                           ("single_integrator_2d", "median"),
+                                           ("double_integrator_2d", 0.02)])
+def test_fused_stein_matches_per_iteration_loop(model_name, bw):
+    """Rollout, score, exact median, fp64 Stein flow and LQR update in one
+    launch vs the per-iteration kernels: the same fp64 arithmetic up to
+    summation order, so trajectories, flow norms, bandwidths and costs agree
+    to ~1e-10."""
+    from paper_2511_11514_b200 import _lib
+    model = getattr(fc, model_name)()
+    s0 = DI_S0 if model.state_dim == 4 else np.array([0.1, 0.1])
+    cfg = fc.PlanConfig(method="stein", eta=0.1, max_iterations=30, convergence_tol=0.0,
+                        metric_interval=0, stein=fc.SteinConfig(bandwidth=bw))
+    disc = fc.Discretization(0.05, 500, s0)
+    a = _plan(True, model, fc.benchmark_mixture(2), disc, cfg)
+    assert "sv_plan_kernel" in _lib.last_kernel() or a.launches < 30 * 4
+    b = _plan(False, model, fc.benchmark_mixture(2), disc, cfg)
+    ra, rb = a.result, b.result
+    assert ra.iterations_used == rb.iterations_used == 30
+    assert rel_inf(ra.trajectory.S, rb.trajectory.S) <= 1e-9
+    assert rel_inf(ra.trajectory.U, rb.trajectory.U) <= 1e-9
+    assert rel_inf(ra.flow_norms, rb.flow_norms) <= 1e-9
+    assert rel_inf(ra.lqr_costs, rb.lqr_costs) <= 1e-9
+    # the bandwidth column of the flow log: the median is exact on both paths
+    assert rel_inf(a.flow_log[:, 1], b.flow_log[:, 1]) <= 1e-9
+    assert ra.phase_times.flow > 0 and ra.phase_times.lqr > 0 and ra.phase_times.rollout > 0
+
+
+def test_fused_stein_stops_on_convergence():
+    model = fc.double_integrator_2d()
+    disc = fc.Discretization(0.05, 400, DI_S0)
+    cfg = fc.PlanConfig(method="stein", eta=0.1, max_iterations=80, convergence_tol=2e-2,
+                        metric_interval=0)
+    a = _plan(True, model, fc.benchmark_mixture(2), disc, cfg).result
+    b = _plan(False, model, fc.benchmark_mixture(2), disc, cfg).result
+    assert a.converged == b.converged
+    assert a.iterations_used == b.iterations_used
+    assert len(a.lqr_costs) == len(b.lqr_costs)
+    assert rel_inf(a.trajectory.S, b.trajectory.S) <= 1e-9
