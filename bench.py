@@ -335,6 +335,7 @@ def run_ours(args):
                 "configs[0]": config1_secondary(torch, fc, flush),
                 "configs[2]": config3_secondary(torch, fc, _dev, peak, flush),
                 "configs[4]": config5_secondary(torch, fc, peak),
+                "configs[4].tsp_baseline": tsp_baseline_secondary(torch, fc),
             }
         if not args.no_cpu:
             sk0 = runs[0][0]
@@ -475,6 +476,25 @@ def config5_secondary(torch, fc, peak, problems=512, iters=100):
                         f"M=4096, {iters} iterations, one batched launch",
             "seconds": t, "problems_per_s": problems / t, "value": pairs / t, "unit": UNIT,
             "frac_of_mufu": pairs / t / peak["ex2"]}
+
+
+def tsp_baseline_secondary(torch, fc, problems=512):
+    """BASELINE configs[4]'s comparison method, the TSP-waypoint baseline
+    (tsp.py:276-316), on the GPU: every tour in one launch, then the tracking
+    rounds per problem (baseline_plans); beside it the reference's own
+    baseline_plan measured on the B200 box's host cores."""
+    m = fc.single_integrator_2d()
+    q = fc.benchmark_mixture(2)
+    disc = fc.Discretization(DT, 1000, np.array([0.1, 0.1]))
+    cfgs = [fc.BaselineConfig(seed=b) for b in range(problems)]
+    _, t = _timed(torch, lambda: fc.baseline_plans(m, q, disc, cfgs), 1)
+    ref = load_json("r02/tsp_baseline_cfg5_gpubox.json") or {}
+    return {"workload": f"TSP-waypoint baseline, {problems} config-5 problems (tour + 10 TV-LQR "
+                        "tracking rounds each), batched tours",
+            "seconds": t, "seconds_per_problem": t / problems,
+            "reference_host": {k: ref.get(k) for k in (
+                "what", "host_cores", "processes", "mean_seconds_per_problem",
+                "problems_per_second_all_processes", "extrapolated_4096_problems_seconds")}}
 
 
 # ---------------------------------------------------------------------------
