@@ -7,12 +7,40 @@ the reference's ownership rules (inputs never mutated, outputs fresh).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import os
 
 import numpy as np
 import torch
 
 from . import _lib
+
+# NVTX ranges around the planner's phases (FCB_NVTX=1), for ncu --nvtx
+# filtering (e.g. --nvtx-include "flow/"); off by default (host cost per range)
+NVTX = os.environ.get("FCB_NVTX", "0") != "0"
+
+
+def nvtx_push(name: str) -> None:
+    if NVTX:
+        torch.cuda.nvtx.range_push(name)
+
+
+def nvtx_pop() -> None:
+    if NVTX:
+        torch.cuda.nvtx.range_pop()
+
+
+@contextlib.contextmanager
+def nvtx(name: str):
+    if not NVTX:
+        yield
+        return
+    torch.cuda.nvtx.range_push(name)
+    try:
+        yield
+    finally:
+        torch.cuda.nvtx.range_pop()
 
 
 def require_cuda() -> torch.device:

@@ -372,6 +372,7 @@ def plan_detailed(
     for it in range(maxit):
         cur = it & 1
         if it == 1 and fused_ok:
+            _dev.nvtx_push("fused_loop")
             fws = _dev.Workspace.get(
                 lib.fcb_plan_fused_workspace_bytes(1, T, M, d, m_c), "plan_fused")
             rc = lib.fcb_plan_fused(
@@ -383,12 +384,14 @@ def plan_detailed(
                 _dev.ptr(warm_valid), _dev.ptr(fstat), state_ptr, _dev.ptr(flow_log),
                 _dev.ptr(lqr_costs), _dev.ptr(phase_ns), 1, maxit, 1, _dev.ptr(upd_ws),
                 _dev.ptr(fws), fws.numel(), stream)
+            _dev.nvtx_pop()
             if rc == _lib.FCB_OK:
                 fused_ran = True
                 break
             if rc != _lib.FCB_ENOTSUP:
                 _lib.check(rc, "fcb_plan_fused")
         if it == 1 and fused_stein_ok:
+            _dev.nvtx_push("fused_loop")
             sws = _dev.Workspace.get(lib.fcb_plan_fused_stein_workspace_bytes(T, d, m_c),
                                      "plan_fused_stein")
             rc = lib.fcb_plan_fused_stein(
@@ -399,6 +402,7 @@ def plan_detailed(
                 log_np1, float(cfg.convergence_tol), _dev.ptr(fstat), state_ptr,
                 _dev.ptr(flow_log), _dev.ptr(lqr_costs), _dev.ptr(phase_ns), 1, maxit,
                 _dev.ptr(upd_ws), _dev.ptr(sws), sws.numel(), stream)
+            _dev.nvtx_pop()
             if rc == _lib.FCB_OK:
                 fused_ran = True
                 break
@@ -408,9 +412,11 @@ def plan_detailed(
             e_prev = torch.cuda.Event(enable_timing=True)
             e_prev.record()
         e0 = e_prev  # the previous iteration's end event
+        _dev.nvtx_push("rollout")
         call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0),
              _dev.ptr(Ubuf[cur]), T, float(disc.dt), _dev.ptr(Sbuf[cur]), d, _dev.ptr(P),
              _dev.ptr(X), None, state_ptr, it, 1, _dev.ptr(roll_ws), stream)
+        _dev.nvtx_pop()
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record()
         e2 = e1
@@ -421,6 +427,7 @@ def plan_detailed(
                  _dev.ptr(yy_cache), _dev.ptr(met_ws), met_ws.numel(), stream)
             e2 = torch.cuda.Event(enable_timing=True)
             e2.record()
+        _dev.nvtx_push("flow")
         if sharded and cfg.method == "sinkhorn":
             shard_flow.flow_into(X, warm_f, warm_p, warm_valid, flow, fstat, state, it, flow_log,
                                  float(cfg.convergence_tol))
@@ -437,15 +444,18 @@ def plan_detailed(
                  _dev.ptr(gmm), bw_fixed, log_np1, _dev.ptr(flow), _dev.ptr(fstat), state_ptr,
                  it, _dev.ptr(flow_log), float(cfg.convergence_tol), _dev.ptr(flow_ws),
                  flow_ws.numel(), stream)
+        _dev.nvtx_pop()
         e3 = torch.cuda.Event(enable_timing=True)
         e3.record()
         # state-independent Jacobians: the Riccati phase is computed once
         lqr_mode = 1 if (linear_model and it > 0) else 0
+        _dev.nvtx_push("lqr")
         call("fcb_plan_update", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(Sbuf[cur]),
              _dev.ptr(Ubuf[cur]), T, float(disc.dt), d, _dev.ptr(P), _dev.ptr(flow),
              _dev.ptr(Q), _dev.ptr(R), float(cfg.eta), _dev.ptr(clamp_d),
              _dev.ptr(Ubuf[1 - cur]), _dev.ptr(lqr_costs), state_ptr, it, lqr_mode,
              _dev.ptr(upd_ws), upd_ws.numel(), stream)
+        _dev.nvtx_pop()
         e4 = torch.cuda.Event(enable_timing=True)
         e4.record()
         e_prev = e4

@@ -168,3 +168,18 @@ def test_plan_is_run_to_run_deterministic():
     b = fc.plan(model, fc.benchmark_mixture(2), disc, cfg)
     assert a.trajectory.S.tobytes() == b.trajectory.S.tobytes()
     assert a.metric_values == b.metric_values
+
+
+def test_plan_with_nvtx_ranges(monkeypatch):
+    """FCB_NVTX=1 wraps the planner phases in NVTX ranges (ncu --nvtx
+    filtering); results are unchanged."""
+    from paper_2511_11514_b200 import _dev
+    model = fc.single_integrator_2d()
+    cfg = fc.PlanConfig(method="sinkhorn", eta=60.0, max_iterations=3, convergence_tol=0.0,
+                        metric_interval=0)
+    disc = fc.Discretization(0.05, 200, np.array([0.1, 0.1]))
+    tg = fc.SamplePoints(fc.benchmark_mixture(2).sample(500, [0, 2]))
+    a = fc.plan(model, tg, disc, cfg)
+    monkeypatch.setattr(_dev, "NVTX", True)
+    b = fc.plan(model, tg, disc, cfg)
+    np.testing.assert_array_equal(a.trajectory.S, b.trajectory.S)
