@@ -38,6 +38,7 @@ from __future__ import annotations
 
 import collections
 import math
+import os
 from typing import Optional
 
 import numpy as np
@@ -67,21 +68,28 @@ def shard_rows(Y: np.ndarray, rank: int, world: int) -> np.ndarray:
 
 
 class Collectives:
-    """The collectives of the sharded schedule, on the current stream."""
+    """The collectives of the sharded schedule, on the current stream.
+
+    At world size 1 they are local copies; FCB_FORCE_COLLECTIVES=1 issues the
+    NCCL calls anyway (a one-rank group), so the stream ordering between the
+    collectives and the device steps is exercised on a single GPU.
+    """
 
     def __init__(self, group=None):
         self.group = group
         self.rank, self.world = _world(group)
+        self.force = (os.environ.get("FCB_FORCE_COLLECTIVES", "0") != "0"
+                      and group is not None and dist.is_initialized())
 
     def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
         """out (world * inp.numel()) <- concatenation of every rank's inp."""
-        if self.world == 1:
+        if self.world == 1 and not self.force:
             out.view(-1)[: inp.numel()].copy_(inp.view(-1))
             return
         dist.all_gather_into_tensor(out.view(-1), inp.contiguous().view(-1), group=self.group)
 
     def all_reduce_sum(self, t: torch.Tensor) -> torch.Tensor:
-        if self.world > 1:
+        if self.world > 1 or self.force:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 

@@ -198,3 +198,23 @@ def test_sharded_median_tiles_R3_equal_exact_median(n, d):
     dev._call("fcb_median_shard_finish", n, math.log(n + 1.0), _dev.ptr(hstat), _dev.ptr(ws),
               None, s)
     assert float(hstat[0]) == O.median_bandwidth(X) == fc.median_bandwidth(X)
+
+
+@pytest.mark.parametrize("method", ["sinkhorn", "stein"])
+def test_forced_nccl_collectives_world1_bit_identical(group1, monkeypatch, method):
+    """FCB_FORCE_COLLECTIVES=1 issues the NCCL all_gather / all_reduce calls of
+    the sharded schedule on the one-rank group (identity operations), so the
+    ordering between NCCL's stream and the device steps on the current stream
+    is exercised on one GPU: the plan must be bit-identical to the local-copy
+    run (a missing wait would read stale gathered buffers)."""
+    m = fc.aircraft_3d()
+    q = fc.benchmark_mixture(3)
+    tg = fc.SamplePoints(q.sample(3000, [0, STREAM_REFERENCE])) if method == "sinkhorn" else q
+    cfg = fc.PlanConfig(method=method, eta=120.0 if method == "sinkhorn" else 0.1,
+                        max_iterations=4, convergence_tol=0.0, metric_interval=0, seed=0)
+    disc = fc.Discretization(0.05, 1500, fc.default_start(m))
+    a = fc.plan_detailed(m, tg, disc, cfg, group=group1)
+    monkeypatch.setenv("FCB_FORCE_COLLECTIVES", "1")
+    b = fc.plan_detailed(m, tg, disc, cfg, group=group1)
+    np.testing.assert_array_equal(a.result.trajectory.S, b.result.trajectory.S)
+    np.testing.assert_array_equal(a.flow_log, b.flow_log)
