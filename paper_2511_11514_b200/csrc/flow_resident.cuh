@@ -151,6 +151,9 @@ struct RsRes {  // combined row partial
 // arrival target is known locally, so an arrival is a fire-and-forget
 // red.release (no atomic round trip) and only the poll waits.
 __shared__ unsigned long long rs_bar_gen;
+#ifndef RS_BAR_SLEEP
+#define RS_BAR_SLEEP 20  // ns between polls of the grid barrier
+#endif
 
 template <bool GRID>
 struct RsGroup {
@@ -166,7 +169,7 @@ struct RsGroup {
                 rs_bar_gen += 1ull;
                 asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&bar->count)
                              : "memory");
-                while (ld_acquire_u64(&bar->count) < target) __nanosleep(20);
+                while (ld_acquire_u64(&bar->count) < target) __nanosleep(RS_BAR_SLEEP);
             }
             __syncthreads();
             FCB_TL_MARK();
