@@ -289,6 +289,134 @@ __device__ void svp_median(const double* __restrict__ X, int n, double log_np1, 
     __syncthreads();
 }
 
+// The flow phase of one iteration over the grid (every CTA): scores of the
+// CTA's points [k0, k1), the bandwidth (exact median or fixed), the Stein flow
+// of those rows and the CTA's sum of |g_i| in npart.  The rows become visible
+// grid-wide at the caller's next barrier.
+template <int D, class Args>
+__device__ void svp_flow_phase(const Args& a, int T, int k0, int k1, const RsGroup<true>& grp,
+                               unsigned& gpass, unsigned& ggather, unsigned* shist, SvpSel& sel,
+                               double* s_h, double* s_rownorm, double* cx, double* cw) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const double* X = a.X;
+    for (int i = k0 + tid; i < k1; i += RS_BLOCK) {
+        double xi[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) xi[q] = __ldcg(X + (size_t)i * D + q);
+        gmm_point<D>(xi, a.k, a.gmm, a.scores + (size_t)i * D, nullptr);
+    }
+    if (a.bw_fixed > 0.0) {
+        if (tid == 0) {
+            const bool clamped = a.bw_fixed <= BANDWIDTH_FLOOR;
+            s_h[0] = clamped ? BANDWIDTH_FLOOR : a.bw_fixed;
+            s_h[1] = NAN;
+            s_h[2] = clamped ? 1.0 : 0.0;
+            s_h[3] = 0.0;
+        }
+        grp.sync();  // scores complete
+    } else {
+        // the first pass's barrier also publishes the scores
+        svp_median<D>(X, T, a.log_np1, a.hist, a.cand, a.ccount, ggather, grp, gpass, shist, sel,
+                      s_h);
+    }
+    // every point as a column, centred on X[0] and scaled by 1/sqrt(h)
+    // (stein_run's form; coincident clouds give x' == 0 exactly)
+    const double h = s_h[0];
+    const double sc = sqrt(1.0 / h), two_h = 2.0 / h;
+    double x0[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) x0[q] = __ldcg(X + q);
+    for (int e = tid; e < T * D; e += RS_BLOCK) {
+        const int q = e % D;
+        const double xc = __ldcg(X + e) - x0[q];
+        cx[e] = xc * sc;
+        cw[e] = __ldcg(a.scores + e) - two_h * xc;
+    }
+    __syncthreads();
+    const double inv_n = 1.0 / T;
+    for (int i = k0 + wid; i < k1; i += RS_WARPS) {
+        double xi[D], K = 0.0, A[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+            xi[q] = cx[(size_t)i * D + q];
+            A[q] = 0.0;
+        }
+        for (int j = lane; j < T; j += 32) {
+            double d2 = 0.0;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                const double df = xi[q] - cx[(size_t)j * D + q];
+                d2 = fma(df, df, d2);
+            }
+            const double kk = exp(-d2);
+            K += kk;
+#pragma unroll
+            for (int q = 0; q < D; ++q) A[q] = fma(kk, cw[(size_t)j * D + q], A[q]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            K += __shfl_xor_sync(0xffffffffu, K, o);
+#pragma unroll
+            for (int q = 0; q < D; ++q) A[q] += __shfl_xor_sync(0xffffffffu, A[q], o);
+        }
+        if (lane == 0) {
+            double sq = 0.0;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                const double xc = __ldcg(X + (size_t)i * D + q) - x0[q];
+                const double g = inv_n * (A[q] + two_h * xc * K);
+                a.flow[(size_t)i * D + q] = g;
+                sq += g * g;
+            }
+            s_rownorm[(i - k0) & 63] = sqrt(sq);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;  // rows in order (at most 64 per CTA, checked on the host)
+        for (int i = k0; i < k1; ++i) s += s_rownorm[(i - k0) & 63];
+        a.npart[grp.rank] = s;
+    }
+}
+
+// After the flow norms are visible: the mean |g| (summed in CTA order by every
+// CTA, so the stop decision is grid-uniform); CTA 0 writes the statistics and
+// planner hooks of stein_finalize_kernel.  Returns the mean.
+template <class Args>
+__device__ double svp_finish_flow(const Args& a, int T, int it, const RsGroup<true>& grp,
+                                  const double* s_h, double* s_mean) {
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int r = 0; r < grp.size; ++r) s += __ldcg(a.npart + r);
+        *s_mean = s / T;
+        if (grp.rank == 0) {
+            const double mm = *s_mean;
+            a.fstat[0] = 0.0;
+            a.fstat[1] = 1.0;
+            a.fstat[2] = 0.0;
+            a.fstat[3] = mm;
+            a.fstat[4] = s_h[0];
+            a.fstat[5] = s_h[2];
+            a.fstat[6] = s_h[1];
+            a.fstat[7] = 0.0;
+            double* lg = a.flow_log + 4 * (size_t)it;
+            lg[0] = mm;
+            lg[1] = s_h[0];
+            lg[2] = s_h[2];
+            lg[3] = s_h[1];
+            a.plan_state[FCB_STATE_FLOWS] = it + 1;
+            if (mm < a.conv_tol) a.plan_state[FCB_STATE_STOP] = 1;
+        }
+    }
+    __syncthreads();
+    return *s_mean;
+}
+
+// Scans spread over the grid as in rs_plan_kernel: CTA r owns steps
+// [T r/G, T (r+1)/G).  (Measured alternative: CTA 0 scanning all T = 500
+// steps of config 1 alone while the others wait -- 40 vs 25 us of LQR per
+// iteration; the block-wide Hillis-Steele over 128 runs is slower than the
+// grid carry.)
 template <int D, class Mdl>
 __global__ void __launch_bounds__(RS_BLOCK, 1) sv_plan_kernel(SvFusedArgs<Mdl::N, Mdl::M> a) {
     constexpr int N = Mdl::N, M = Mdl::M;
@@ -301,7 +429,7 @@ __global__ void __launch_bounds__(RS_BLOCK, 1) sv_plan_kernel(SvFusedArgs<Mdl::N
     __shared__ unsigned shist[2 * SVP_BINS];
     __shared__ SvpSel sel;
     PfSmem<N>& sm = *reinterpret_cast<PfSmem<N>*>(rs_smem);
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int tid = threadIdx.x;
     RsArgs ep{};
     ep.bar = a.bar;
     ep.done = a.done;
@@ -313,16 +441,17 @@ __global__ void __launch_bounds__(RS_BLOCK, 1) sv_plan_kernel(SvFusedArgs<Mdl::N
     if (*((volatile const int*)plan_state) != 0) return;  // uniform: set before the launch
     if (tid == 0) phigam_compute<Mdl>(pf.prm + 0, pf.dt, s_pg);
     double* dff = pf.dff;
-    double* flow = a.flow;
     double* X = a.X;
-    const LiftedFlow<N> lift{flow, pf.P, pf.d};
+    unsigned gpass = 0, ggather = 0;
+    const PfChunk chF = pf_chunk<true, true>(T, grp);  // this CTA's points / steps
+    double* cx = reinterpret_cast<double*>(reinterpret_cast<char*>(rs_smem) + a.sv_off);
+    double* cw = cx + (size_t)T * D;
+    unsigned long long tr = 0, tf = 0, tl = 0;
+    const LiftedFlow<N> lift{a.flow, pf.P, pf.d};
     bool first = true;
     bool pending_finish = false;
     int pending_it = 0;
-    unsigned gpass = 0, ggather = 0;
-    const PfChunk chF = pf_chunk<true, true>(T, grp);
     const PfChunk chB = pf_chunk<false, true>(T, grp);
-    unsigned long long tr = 0, tf = 0, tl = 0;
     // this CTA's Riccati arrays in shared memory (as rs_plan_kernel)
     const double* rAcl = pf.Acl;
     const double* rK = pf.K;
@@ -352,15 +481,13 @@ __global__ void __launch_bounds__(RS_BLOCK, 1) sv_plan_kernel(SvFusedArgs<Mdl::N
         rGm = sGm - chF.k0;
         rstride = cnt;
     }
-    double* cx = reinterpret_cast<double*>(reinterpret_cast<char*>(rs_smem) + a.sv_off);
-    double* cw = cx + (size_t)T * D;
     __syncthreads();
     for (int it = pf.it0; it < pf.maxit; ++it) {
         double* U = ((it & 1) ? pf.U1 : pf.U0);
         double* Un = ((it & 1) ? pf.U0 : pf.U1);
         double* S = ((it & 1) ? pf.S1 : pf.S0);
         const unsigned long long t0 = pf_clock();
-        // ---- rollout of U (dynamics.py:276-312) -> S, X -------------------
+        // ---- rollout of U (dynamics.py:276-312) -> S, X ---------------
         if (tid == 0) s_first_bad = 0x7f7f7f7f;
         {
             const RollMap<N, M> mapf{s_pg, U};
@@ -386,119 +513,16 @@ __global__ void __launch_bounds__(RS_BLOCK, 1) sv_plan_kernel(SvFusedArgs<Mdl::N
             }
         }
         const unsigned long long t1 = pf_clock();
-        // ---- Stein flow (stein.py:79-122) ---------------------------------
-        for (int i = chF.k0 + tid; i < chF.k1; i += RS_BLOCK) {
-            double xi[D];
-#pragma unroll
-            for (int q = 0; q < D; ++q) xi[q] = __ldcg(X + (size_t)i * D + q);
-            gmm_point<D>(xi, a.k, a.gmm, a.scores + (size_t)i * D, nullptr);
-        }
-        if (a.bw_fixed > 0.0) {
-            if (tid == 0) {
-                const bool clamped = a.bw_fixed <= BANDWIDTH_FLOOR;
-                s_h[0] = clamped ? BANDWIDTH_FLOOR : a.bw_fixed;
-                s_h[1] = NAN;
-                s_h[2] = clamped ? 1.0 : 0.0;
-                s_h[3] = 0.0;
-            }
-            grp.sync();  // scores complete
-        } else {
-            // the first pass's barrier also publishes the scores
-            svp_median<D>(X, T, a.log_np1, a.hist, a.cand, a.ccount, ggather, grp, gpass, shist,
-                          sel, s_h);
-        }
-        {
-            // every point as a column, centred on X[0] and scaled by 1/sqrt(h)
-            // (stein_run's form; coincident clouds give x' == 0 exactly)
-            const double h = s_h[0];
-            const double sc = sqrt(1.0 / h), two_h = 2.0 / h;
-            double x0[D];
-#pragma unroll
-            for (int q = 0; q < D; ++q) x0[q] = __ldcg(X + q);
-            for (int e = tid; e < T * D; e += RS_BLOCK) {
-                const int q = e % D;
-                const double xc = __ldcg(X + e) - x0[q];
-                cx[e] = xc * sc;
-                cw[e] = __ldcg(a.scores + e) - two_h * xc;
-            }
-            __syncthreads();
-            const double inv_n = 1.0 / T;
-            for (int i = chF.k0 + wid; i < chF.k1; i += RS_WARPS) {
-                double xi[D], K = 0.0, A[D];
-#pragma unroll
-                for (int q = 0; q < D; ++q) {
-                    xi[q] = cx[(size_t)i * D + q];
-                    A[q] = 0.0;
-                }
-                for (int j = lane; j < T; j += 32) {
-                    double d2 = 0.0;
-#pragma unroll
-                    for (int q = 0; q < D; ++q) {
-                        const double df = xi[q] - cx[(size_t)j * D + q];
-                        d2 = fma(df, df, d2);
-                    }
-                    const double kk = exp(-d2);
-                    K += kk;
-#pragma unroll
-                    for (int q = 0; q < D; ++q) A[q] = fma(kk, cw[(size_t)j * D + q], A[q]);
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    K += __shfl_xor_sync(0xffffffffu, K, o);
-#pragma unroll
-                    for (int q = 0; q < D; ++q) A[q] += __shfl_xor_sync(0xffffffffu, A[q], o);
-                }
-                if (lane == 0) {
-                    double sq = 0.0;
-#pragma unroll
-                    for (int q = 0; q < D; ++q) {
-                        const double xc = __ldcg(X + (size_t)i * D + q) - x0[q];
-                        const double g = inv_n * (A[q] + two_h * xc * K);
-                        flow[(size_t)i * D + q] = g;
-                        sq += g * g;
-                    }
-                    s_rownorm[(i - chF.k0) & 63] = sqrt(sq);
-                }
-            }
-            __syncthreads();
-            if (tid == 0) {
-                double s = 0.0;  // rows in order (at most 64 per CTA, checked on the host)
-                for (int i = chF.k0; i < chF.k1; ++i) s += s_rownorm[(i - chF.k0) & 63];
-                a.npart[grp.rank] = s;
-            }
-        }
+        // ---- Stein flow (stein.py:79-122) -----------------------------
+        svp_flow_phase<D>(a, T, chF.k0, chF.k1, grp, gpass, ggather, shist, sel, s_h,
+                          s_rownorm, cx, cw);
         const unsigned long long t2 = pf_clock();
-        // ---- LQR affine phase (lqr.py:180-200 on the stored Riccati phase) ---
+        // ---- LQR affine phase (lqr.py:180-200 on the stored Riccati phase)
         if (tid == 0) s_fail = -1;
         const EtaMap<N, LiftedFlow<N>> emap{rAcl, pf.Q, pf.dt, rstride, lift};
         const AMap<N>* incE = pf_phase1<N, false>(T, chB, emap, sm, pf.agg);
         grp.sync();  // flow norms visible
-        if (tid == 0) {
-            double s = 0.0;
-            for (int r = 0; r < grp.size; ++r) s += __ldcg(a.npart + r);
-            s_mean = s / T;
-            if (grp.rank == 0) {
-                // stein_finalize_kernel's statistics and planner hooks
-                const double mm = s_mean;
-                a.fstat[0] = 0.0;
-                a.fstat[1] = 1.0;
-                a.fstat[2] = 0.0;
-                a.fstat[3] = mm;
-                a.fstat[4] = s_h[0];
-                a.fstat[5] = s_h[2];
-                a.fstat[6] = s_h[1];
-                a.fstat[7] = 0.0;
-                double* lg = a.flow_log + 4 * (size_t)it;
-                lg[0] = mm;
-                lg[1] = s_h[0];
-                lg[2] = s_h[2];
-                lg[3] = s_h[1];
-                plan_state[FCB_STATE_FLOWS] = it + 1;
-                if (mm < a.conv_tol) plan_state[FCB_STATE_STOP] = 1;
-            }
-        }
-        __syncthreads();
-        if (s_mean < a.conv_tol) break;  // converged: no update (optimizer.py:251-255)
+        if (svp_finish_flow(a, T, it, grp, s_h, &s_mean) < a.conv_tol) break;
         {
             const EtaOut<N, M> eout{rLg, dff, &s_fail, rstride};
             pf_phase2<N, false, true>(T, chB, emap, eout, nullptr, sm, incE, pf.agg);

@@ -167,3 +167,4 @@ def test_fused_stein_stops_on_convergence():
     assert a.iterations_used == b.iterations_used
     assert len(a.lqr_costs) == len(b.lqr_costs)
     assert rel_inf(a.trajectory.S, b.trajectory.S) <= 1e-9
+
