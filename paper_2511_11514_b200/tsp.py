@@ -232,7 +232,10 @@ def track_waypoints(model: DynamicsModel, waypoints, T: int, dt: float, iteratio
     state = torch.zeros(8, dtype=torch.int32, device=dev)
     roll_ws = _dev.Workspace.get(lib.fcb_rollout_workspace_bytes(n_s, T), "track_roll")
     upd_ws = _dev.Workspace.get(lib.fcb_plan_update_workspace_bytes(n_s, m_c, T), "track_upd")
-    method = rollout_method(T)
+    # tracking rounds: the parallel-in-time rollout (as plan()'s loop); the
+    # returned trajectory: the final rollout's method (sequential, bit-exact
+    # with numpy for polynomial models, up to SEQUENTIAL_ROLLOUT_MAX_T)
+    method_final = rollout_method(T)
 
     def call(name, *args):
         _lib.check(getattr(lib, name)(*args), name)
@@ -242,7 +245,7 @@ def track_waypoints(model: DynamicsModel, waypoints, T: int, dt: float, iteratio
         ev[2 * it].record()
         call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0d),
              _dev.ptr(Ub[it & 1]), T, float(dt), _dev.ptr(S), d, _dev.ptr(P), _dev.ptr(X), None,
-             _dev.ptr(state), it, method, _dev.ptr(roll_ws), st)
+             _dev.ptr(state), it, 1, _dev.ptr(roll_ws), st)
         ev[2 * it + 1].record()
         torch.sub(ref, X, out=err)  # the tracking error is the flow the update steers by
         call("fcb_plan_update", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(S),
@@ -254,8 +257,8 @@ def track_waypoints(model: DynamicsModel, waypoints, T: int, dt: float, iteratio
     status = torch.empty(1, dtype=torch.int32, device=dev)
     ev[2 * iterations].record()
     call("fcb_rollout", spec.model_id, n_s, m_c, _dev.ptr(prm), _dev.ptr(s0d), _dev.ptr(U_fin),
-         T, float(dt), _dev.ptr(S), d, _dev.ptr(P), _dev.ptr(X), _dev.ptr(status), None, 0, method,
-         _dev.ptr(roll_ws), st)
+         T, float(dt), _dev.ptr(S), d, _dev.ptr(P), _dev.ptr(X), _dev.ptr(status), None, 0,
+         method_final, _dev.ptr(roll_ws), st)
     ev[2 * iterations + 1].record()
     ev[-1].synchronize()
     code = state.cpu().numpy()

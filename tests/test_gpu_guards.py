@@ -229,3 +229,61 @@ def test_sharded_step_guards():
                                    flow.ptr, fstat.ptr, None, 0, None, 0.0, w.ptr, w.view.numel(),
                                    _dev.stream()), "combine")
     check(flow, fstat, w)
+
+
+def test_cached_divergence_guards():
+    rng = np.random.default_rng(8)
+    n, m, d = 413, 977, 2
+    Xd, Yd = _dev.f64(rng.random((n, d))), _dev.f64(rng.random((m, d)))
+    L = lib()
+    out, cache = Guarded((4,)), Guarded((5,), init=np.zeros(5))
+    w = ws(L.fcb_sinkhorn_divergence_workspace_bytes(0, n, m, d))
+    for _ in range(2):  # miss, then hit
+        _lib.check(L.fcb_sinkhorn_divergence_cached(0, _dev.ptr(Xd), n, _dev.ptr(Yd), m, d, 0.05,
+                                                    200, 1e-6, out.ptr, None, cache.ptr, w.ptr,
+                                                    w.view.numel(), _dev.stream()), "div_cached")
+        check(out, cache, w)
+    assert float(cache.view[4]) == 1.0
+
+
+@pytest.mark.parametrize("T,bw", [(517, 0.0), (131, 0.03)])
+def test_fused_stein_planner_guards(T, bw):
+    """fcb_plan_fused_stein (sv_plan_kernel) with every output guarded, on
+    the stored Riccati phase of a mode-0 update (as plan() runs it)."""
+    model = fc.double_integrator_2d()
+    spec = device_model(model)
+    ns, mc, d = model.state_dim, model.control_dim, model.workspace_dim
+    L = lib()
+    dev = _dev.require_cuda()
+    prm = spec.device_params(dev)
+    q = fc.benchmark_mixture(2)
+    s0 = _dev.f64(np.array([0.1, 0.1, 0.0, 0.0]))
+    P = _dev.f64(model.project_matrix)
+    wts = fc.workspace_weights(model.project_matrix, mc)
+    Q, R = _dev.f64(wts.Q), _dev.f64(wts.R)
+    maxit = 4
+    U0 = Guarded((T, mc), init=1e-2 * np.random.default_rng(T).standard_normal((T, mc)))
+    U1, S0, S1 = Guarded((T, mc)), Guarded((T + 1, ns)), Guarded((T + 1, ns))
+    X, flow = Guarded((T, d)), Guarded((T, d))
+    fstat, state = Guarded((8,)), Guarded((8,), torch.int32, np.zeros(8))
+    flow_log, costs = Guarded((maxit, 4)), Guarded((maxit,))
+    phase = Guarded((3,), torch.int64, np.zeros(3))
+    upd = ws(L.fcb_plan_update_workspace_bytes(ns, mc, T))
+    scratch = torch.zeros(8, dtype=torch.int32, device="cuda")
+    z = lambda *s: _dev.zeros(s)  # noqa: E731
+    _lib.check(L.fcb_plan_update(spec.model_id, ns, mc, _dev.ptr(prm), _dev.ptr(z(T + 1, ns)),
+                                 _dev.ptr(z(T, mc)), T, 0.05, d, _dev.ptr(P), _dev.ptr(z(T, d)),
+                                 _dev.ptr(Q), _dev.ptr(R), 0.1, None, _dev.ptr(z(T, mc)),
+                                 _dev.ptr(z(maxit)), _dev.ptr(scratch), 0, 0, upd.ptr,
+                                 upd.view.numel(), _dev.stream()), "plan_update")
+    w = ws(L.fcb_plan_fused_stein_workspace_bytes(T, d, mc))
+    rc = L.fcb_plan_fused_stein(spec.model_id, ns, mc, _dev.ptr(prm), _dev.ptr(s0), U0.ptr, U1.ptr,
+                                S0.ptr, S1.ptr, T, 0.05, d, _dev.ptr(P), X.ptr, flow.ptr,
+                                _dev.ptr(Q), _dev.ptr(R), 0.1, None, q.num_components,
+                                _dev.ptr(q.device_params()), bw, math.log(T + 1.0), 0.0,
+                                fstat.ptr, state.ptr, flow_log.ptr, costs.ptr, phase.ptr, 1, maxit,
+                                upd.ptr, w.ptr, w.view.numel(), _dev.stream())
+    _lib.check(rc, "plan_fused_stein")
+    check(U0, U1, S0, S1, X, flow, fstat, state, flow_log, costs, phase, upd, w)
+    st = state.view.cpu().numpy()
+    assert st[0] == 0 and st[4] == maxit and st[5] == maxit  # flows, updates
