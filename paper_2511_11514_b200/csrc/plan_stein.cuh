@@ -6,12 +6,14 @@
 //   rollout   affine scan of s_{k+1} = Phi s_k + Gam u_k -> S, X = P S[1:]
 //             (plan_fused.cuh's pf_phase1/2, CTA r owns steps [T r/G, T (r+1)/G))
 //   score     GaussianMixture score of the CTA's own points (reference.py:103-110)
-//   bandwidth exact median of all T^2 distances, 6 radix passes over the
+//   bandwidth exact median of all T^2 distances by radix passes over the
 //             grid: every CTA histograms its run of the T (T-1) / 2 pairs in
 //             shared memory, adds the nonzero bins into a rotating global
 //             histogram, and after the barrier every CTA selects the digit
 //             from the global counts itself (identical inputs, identical
-//             prefixes: no broadcast barrier); h = med^2 / log(T+1)
+//             prefixes: no broadcast barrier); once the selected bucket holds
+//             <= SVP_CAND keys (after two passes at config 1) they are
+//             gathered and ranked exactly; h = med^2 / log(T+1)
 //   flow      g_i = (1/T)[sum_j k_ij s_j + (2/h)(x_i sum_j k_ij - sum_j k_ij x_j)]
 //             for the CTA's own rows against all T points in shared memory
 //             (fp64, the per-iteration path's centred / scaled form)
